@@ -1,0 +1,146 @@
+/*
+ * zk.h -- C ABI of libzk, the B200 (sm_100a) complex128 Krylov hot path.
+ *
+ * This is the drop-in boundary for the reference package `zlinalg`
+ * (/root/reference/pkg/src/zlinalg).  The reference has no FFI of its own:
+ * its hot path is the Python module API exported at `__init__.py:8-91`, and
+ * each entry point below replaces one of those functions (cited per
+ * function).  INTEGRATION.md shows the ctypes binding a maintainer would add
+ * to `vecops.py`, `sparse.py` and `krylov.py`; paper_2112_06465_b200/ is that
+ * binding, packaged.
+ *
+ * Conventions
+ *  - Plain C types only.  Complex vectors are device pointers to interleaved
+ *    little-endian binary64 (re, im) pairs, i.e. numpy complex128 / `<c16`
+ *    (cnum.py:1-8, vecops.py:203-207).  Host pointers are marked `_host`.
+ *  - Every function returns a zk_status.  Nothing throws across the ABI;
+ *    zk_last_error() returns a thread-local message for the last failure.
+ *    Status codes map 1:1 onto the reference's exception classes
+ *    (errors.py:4-39).
+ *  - Argument checks (lengths, indices, parameters) run before any device
+ *    work is enqueued, so a failed call never writes an output
+ *    (test_vecops.py:110-125: "raises before any write").
+ *  - All work is ordered on the context's stream.  Calls returning host
+ *    scalars (zdotc/znorm2/bicgstab) synchronise; the others are async.
+ *  - Arithmetic reproduces the reference bit for bit: numpy's complex
+ *    multiply formula, numpy's pairwise summation order inside each
+ *    reduction block, the left fold over blocks and Python's scalar
+ *    recurrences.  zk_set_arith() selects the host
+ *    numpy fingerprint being reproduced.
+ */
+#ifndef ZK_H
+#define ZK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int zk_status;
+#define ZK_OK 0
+#define ZK_ERR_DIMENSION 1   /* errors.DimensionError */
+#define ZK_ERR_FORMAT 2      /* errors.FormatError */
+#define ZK_ERR_PARAMETER 3   /* errors.ParameterError */
+#define ZK_ERR_SINGULAR 4    /* errors.SingularPreconditionerError */
+#define ZK_ERR_BREAKDOWN 5   /* errors.BreakdownError (report still filled) */
+#define ZK_ERR_CUDA 6        /* device / driver failure */
+#define ZK_ERR_NOMEM 7       /* device allocation failed */
+#define ZK_ERR_NODEVICE 8    /* no CUDA device: there is no CPU fallback */
+
+#define ZK_MODE_BLOCKED 0    /* vecops.BLOCKED */
+#define ZK_MODE_SEQUENTIAL 1 /* vecops.SEQUENTIAL */
+
+typedef struct zk_context zk_context;
+typedef struct zk_csr zk_csr;
+
+/* ---- context, memory ---------------------------------------------------- */
+const char* zk_last_error(void);
+const char* zk_version(void);
+zk_status zk_context_create(int device, zk_context** out);
+zk_status zk_context_destroy(zk_context* ctx);
+/* Fingerprint of the numpy being reproduced: use_fma=1 is the AVX512F/FMA3
+ * complex multiply (fma(a.re,b.re,-(a.im*b.im)), fma(a.re,b.im,a.im*b.re)),
+ * 0 the plain one; elide_bytes is numpy's temporary-elision threshold
+ * (NPY_MIN_ELIDE_BYTES, 256 KiB) that swaps SpMV's product operands. */
+zk_status zk_set_arith(zk_context* ctx, int use_fma, int64_t elide_bytes);
+zk_status zk_malloc(zk_context* ctx, size_t bytes, void** dptr);
+zk_status zk_free(zk_context* ctx, void* dptr);
+zk_status zk_host_alloc(size_t bytes, void** hptr);   /* pinned */
+zk_status zk_host_free(void* hptr);
+zk_status zk_memcpy_h2d(zk_context* ctx, void* dst, const void* src_host, size_t bytes);
+zk_status zk_memcpy_d2h(zk_context* ctx, void* dst_host, const void* src, size_t bytes);
+zk_status zk_memcpy_d2d(zk_context* ctx, void* dst, const void* src, size_t bytes);
+zk_status zk_memset(zk_context* ctx, void* dst, int value, size_t bytes);
+zk_status zk_synchronize(zk_context* ctx);
+/* Kernels launched by this context so far (graph nodes included). */
+zk_status zk_launch_count(zk_context* ctx, int64_t* count);
+/* Launch stream as an opaque handle (cudaStream_t) for event timing. */
+zk_status zk_stream(zk_context* ctx, void** stream);
+
+/* ---- level-1 kernels (vecops.py) ---------------------------------------- */
+/* zscal: x <- F1(x, alpha)                      replaces vecops.zscal  (vecops.py:124-127) */
+zk_status zk_zscal(zk_context* ctx, int64_t n, double alpha_re, double alpha_im, double* x);
+/* zaxpy: y <- y + F1(alpha, x)                  replaces vecops.zaxpy  (vecops.py:130-134) */
+zk_status zk_zaxpy(zk_context* ctx, int64_t n, double alpha_re, double alpha_im,
+                   const double* x, double* y);
+/* zaxmy: y <- F1(y, x)                          replaces vecops.zaxmy  (vecops.py:137-141) */
+zk_status zk_zaxmy(zk_context* ctx, int64_t n, const double* x, double* y);
+/* zassign: dst <- src                           replaces vecops.zassign (vecops.py:117-121) */
+zk_status zk_zassign(zk_context* ctx, int64_t n, double* dst, const double* src);
+/* out <- F1(v, minv)                   replaces Preconditioner.apply (krylov.py:92-100) */
+zk_status zk_jacobi_apply(zk_context* ctx, int64_t n, const double* v, const double* minv, double* out);
+/* sum cbar(x)*y, cbar = conj when conjugate; block_size in [64, 65536] (power of
+ * two) with mode BLOCKED, or mode SEQUENTIAL.  result_host = (re, im).
+ *                                                replaces vecops.zdot (vecops.py:165-186) */
+zk_status zk_zdotc(zk_context* ctx, int64_t n, const double* x, const double* y, int conjugate,
+                   int64_t block_size, int mode, double* result_host);
+/*                                                replaces vecops.znorm2 (vecops.py:189-200) */
+zk_status zk_znorm2(zk_context* ctx, int64_t n, const double* x, int64_t block_size, int mode,
+                    double* result_host);
+
+/* ---- CSR matrix and SpMV (sparse.py) ------------------------------------ */
+/* Upload a validated CSR (zero-based int64 ia[n_rows+1], ja[nnz]; complex128
+ * aa[nnz]; strictly increasing columns per row -- CsrMatrix._validate,
+ * sparse.py:79-103) into the device SELL-32 layout.  Host pointers.
+ *                                   device twin of CsrMatrix (sparse.py:60-158) */
+zk_status zk_csr_create(zk_context* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                        const int64_t* ia_host, const int64_t* ja_host, const double* aa_host,
+                        zk_csr** out);
+/* Same, from device-resident CSR arrays (ia/ja int64, aa complex128). */
+zk_status zk_csr_create_device(zk_context* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                               const int64_t* ia, const int64_t* ja, const double* aa,
+                               zk_csr** out);
+zk_status zk_csr_destroy(zk_csr* A);
+/* Device bytes held by the matrix (SELL arrays incl. padding). */
+zk_status zk_csr_bytes(const zk_csr* A, int64_t* bytes, int64_t* padded_elems);
+/* y <- A x (x: n_cols, y: n_rows)               replaces sparse.spmv (sparse.py:217-232) */
+zk_status zk_spmv(zk_context* ctx, const zk_csr* A, const double* x, double* y);
+
+/* ---- BiCGStab (krylov.py) ----------------------------------------------- */
+typedef struct {
+    int64_t iterations;          /* SolveReport.iterations */
+    int32_t converged;           /* SolveReport.converged */
+    int32_t breakdown;           /* 0 none, 1 rho, 2 omega, 3 shadow pivot, 4 <t,t> */
+    double final_relative_residual;
+    int64_t history_len;         /* iterations + 1 (entries written to history_host) */
+    int64_t kernel_launches;     /* kernels launched by this solve */
+} zk_solve_report;
+
+/* Right-preconditioned BiCGStab, device-resident: x, r, r~, p, v, s, t, p^,
+ * s^ never leave HBM and the host waits once, for the final report.
+ * b: device rhs; minv: device inverse diagonal (Jacobi) or NULL (identity);
+ * x0: device initial guess or NULL (zero); x_out: device solution (n).
+ * history_host: >= max_iterations + 1 doubles.
+ * Returns ZK_OK (converged or not: non-convergence is data, krylov.py:295)
+ * or ZK_ERR_BREAKDOWN with the report filled up to the breakdown.
+ *                              replaces krylov.solve_bicgstab (krylov.py:213-295) */
+zk_status zk_bicgstab(zk_context* ctx, const zk_csr* A, const double* b, const double* minv,
+                      const double* x0, double tolerance, int64_t max_iterations, double* x_out,
+                      double* history_host, zk_solve_report* report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZK_H */

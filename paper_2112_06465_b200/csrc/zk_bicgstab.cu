@@ -1,0 +1,575 @@
+// zk_bicgstab.cu -- device-resident right-preconditioned BiCGStab
+// (krylov.py:213-295, _Run krylov.py:139-206), bitwise faithful.
+//
+// One iteration of the reference (op order in SURVEY 3.2) is fused into five
+// grid-wide phases, every vector pass doing all the elementwise work and the
+// reduction that follows it:
+//
+//   K2  v = A p^            + block partials of <r~, v>    -> fold: pivot, alpha
+//   K3  s = r - alpha v, s^ = M s, |s|^2 partials           -> fold: s-check
+//  [K3x x += alpha p^ ; K6x ||b - A x||  -- only when the s-check fires]
+//   K4  t = A s^            + <t,t>, <t,s> partials         -> fold: omega
+//   K5  x = (x + alpha p^) + omega s^, r = s - omega t,
+//       <r~, r> partials                                    -> fold: rho', beta
+//   K61 ||b - A x|| partials (true residual, _Run.true_relative_residual)
+//       fused with next iteration's p = ((p - omega v) * beta) + r, p^ = M p
+//                                                           -> fold: record, stop?
+//
+// Each phase is one kernel of one CTA per 4096-row block; the last CTA to
+// finish folds the block partials in order and runs the scalar recurrences
+// (Python Cplx arithmetic, zk_common.cuh) on a device SolverState.  The loop
+// is a CUDA-graph conditional WHILE node whose condition K61 sets, so a
+// whole solve is one graph launch and the host synchronises once.
+#include <cstdlib>
+#include <cstring>
+
+#include "zk_internal.h"
+#include "zk_spmv.cuh"
+
+namespace zk {
+
+SellView sell_view(const zk_csr* A, const zk_context* c);
+size_t reduce_smem_bytes(int nnodes, int nacc, size_t vbytes, int64_t fold_chunk);
+int plan_nnodes(zk_context* c, int32_t L, int32_t kind);
+
+enum : int32_t { ST_RUNNING = 0, ST_CONVERGED = 1, ST_NOT_CONVERGED = 2, ST_BREAKDOWN = 3 };
+enum : int32_t { BD_NONE = 0, BD_RHO = 1, BD_OMEGA = 2, BD_PIVOT = 3, BD_TT = 4 };
+
+struct SolverState {
+    double2 rho, rho_old, alpha, omega, beta;
+    double b_norm, tol, last_rel;
+    int64_t maxit, iterations, trips;
+    int32_t done, status, what, scheck, alpha_applied, trivial_zero;
+    unsigned int counter;
+    int32_t pad;
+};
+
+struct SolverBufs {
+    double2 *x, *b, *minv, *r, *rs, *p, *v, *s, *t, *ph, *sh;
+    double* partials;  // nblocks * 4 doubles
+    double* hist;      // hist_cap doubles
+    SolverState* st;
+    int64_t n, nblocks;
+    bool jacobi, fma;
+};
+
+constexpr int kStashBytes = kBlock * sizeof(double2);  // 64 KiB
+constexpr int kNodeBytes = 8 * 1024;                   // plan nodes (<= 129 nodes x 2 acc x 16 B)
+constexpr int kSpmvSmem = kStashBytes + kNodeBytes;
+constexpr int kEwSmem = 32 * 1024 + kNodeBytes;        // fold scratch (2048 x 16 B) + nodes
+
+struct SolverPlan {
+    int64_t n = 0;
+    bool jacobi = false;
+    int64_t hist_cap = 0;
+    SolverBufs bufs{};
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool graph_ok = false;
+};
+
+namespace {
+
+__device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
+
+__device__ __forceinline__ void stop(SolverState* st, int32_t status, int32_t what) {
+    st->status = status;
+    st->what = what;
+    st->done = 1;
+}
+
+// K1 body for one element: p = ((p + F1(-w, v)) * beta) + F1(1, r); p^ = F1(p, minv)
+// (krylov.py:263-266; zaxpy, zscal, zaxpy, M.apply -- three separate roundings).
+__device__ __forceinline__ void p_update(const SolverBufs& B, double2 mw, double2 beta, int64_t i) {
+    const bool fma = B.fma;
+    double2 p = B.p[i];
+    p = cadd(p, f1(mw, B.v[i], fma));
+    p = f1(p, beta, fma);
+    p = cadd(p, f1(make_double2(1.0, 0.0), B.r[i], fma));
+    B.p[i] = p;
+    if (B.jacobi) B.ph[i] = f1(p, __ldg(B.minv + i), fma);
+}
+
+// ---- setup: r0 = b - A x0, ||b||, ||r0||, <r0, r0> (krylov.py:159-168, 255) ----
+__global__ void __launch_bounds__(kThreads) k_setup(SellView A, SolverBufs B, PlanPtrs pc, PlanPtrs pr) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* stash = reinterpret_cast<double2*>(smem);
+    SolverState* st = B.st;
+    if (st->done) return;
+    const int64_t blk = blockIdx.x, base = blk * kBlock;
+    const bool fma = B.fma;
+    auto epi = [&](int64_t row, double2 ax) {
+        double2 r0 = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, fma));
+        B.r[row] = r0;
+        B.rs[row] = r0;
+        stash[row - base] = r0;
+    };
+    spmv_block(A, B.x, blk, epi);
+    __syncthreads();
+    double* nodes_r = reinterpret_cast<double*>(smem + kStashBytes);
+    auto fr = [&](int64_t e, double (&v)[2]) {
+        v[0] = abs2_np(B.b[e]);
+        v[1] = abs2_np(stash[e - base]);
+    };
+    double outr[2];
+    block_reduce<double, 2>(pr, B.n, kBlock, blk, fr, nodes_r, outr);
+    double2* nodes_c = reinterpret_cast<double2*>(smem + kStashBytes);
+    auto fc = [&](int64_t e, double2 (&v)[1]) {
+        double2 r0 = stash[e - base];
+        v[0] = f1(conjz(r0), r0, fma);
+    };
+    double2 outc[1];
+    block_reduce<double2, 1>(pc, B.n, kBlock, blk, fc, nodes_c, outc);
+    double* P = B.partials;
+    double2* PC = reinterpret_cast<double2*>(P + 2 * B.nblocks);
+    if (threadIdx.x == 0) {
+        P[2 * blk] = outr[0];
+        P[2 * blk + 1] = outr[1];
+        PC[blk] = outc[0];
+    }
+    if (!arrive_last(&st->counter, gridDim.x)) return;
+    double tr[2];
+    ordered_fold<double>(P, 2, B.nblocks, reinterpret_cast<double*>(smem), 4096, tr);
+    double2 tc;
+    ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &tc);
+    if (threadIdx.x != 0) return;
+    st->counter = 0;
+    const double bn = __dsqrt_rn(tr[0]), rn = __dsqrt_rn(tr[1]);
+    st->b_norm = bn;
+    const double h0 = bn > 0.0 ? __ddiv_rn(rn, bn) : 0.0;
+    B.hist[0] = h0;
+    st->last_rel = h0;
+    if (bn == 0.0) {  // trivial_result: zero rhs -> x = 0, history [0.0]
+        B.hist[0] = 0.0;
+        st->last_rel = 0.0;
+        st->trivial_zero = 1;
+        stop(st, ST_CONVERGED, BD_NONE);
+        return;
+    }
+    if (h0 <= st->tol) {  // initial guess already solves
+        stop(st, ST_CONVERGED, BD_NONE);
+        return;
+    }
+    // iteration 1: rho = alpha = omega = 1, no breakdown possible
+    const double2 one = make_double2(1.0, 0.0);
+    st->rho_old = one;
+    st->alpha = one;
+    st->omega = one;
+    st->beta = cmul_py(cdiv_py(tc, one), cdiv_py(one, one));
+    st->rho = tc;
+}
+
+// ---- K1: p update for the first iteration (p = v = 0) ----
+__global__ void __launch_bounds__(kThreads) k_p_first(SolverBufs B) {
+    const SolverState* st = B.st;
+    if (st->done) return;
+    const double2 mw = neg(st->omega), beta = st->beta;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride) p_update(B, mw, beta, i);
+}
+
+// ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
+__global__ void __launch_bounds__(kThreads) k_spmv_pivot(SellView A, SolverBufs B, PlanPtrs pc) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* stash = reinterpret_cast<double2*>(smem);
+    SolverState* st = B.st;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;
+    if (st->done) return;
+    const int64_t blk = blockIdx.x, base = blk * kBlock;
+    const bool fma = B.fma;
+    auto epi = [&](int64_t row, double2 av) {
+        B.v[row] = av;
+        stash[row - base] = av;
+    };
+    spmv_block(A, B.ph, blk, epi);
+    __syncthreads();
+    double2* nodes = reinterpret_cast<double2*>(smem + kStashBytes);
+    auto f = [&](int64_t e, double2 (&v)[1]) { v[0] = f1(conjz(__ldg(B.rs + e)), stash[e - base], fma); };
+    double2 out[1];
+    block_reduce<double2, 1>(pc, B.n, kBlock, blk, f, nodes, out);
+    double2* PC = reinterpret_cast<double2*>(B.partials);
+    if (threadIdx.x == 0) PC[blk] = out[0];
+    if (!arrive_last(&st->counter, gridDim.x)) return;
+    double2 pivot;
+    ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &pivot);
+    if (threadIdx.x != 0) return;
+    st->counter = 0;
+    if (small_py(pivot)) {
+        stop(st, ST_BREAKDOWN, BD_PIVOT);
+        return;
+    }
+    st->alpha = cdiv_py(st->rho, pivot);
+}
+
+// ---- K3: s = r + F1(-alpha, v); s^ = M s; ||s|| -> s-check (krylov.py:272-275) ----
+__global__ void __launch_bounds__(kThreads) k_s_update(SolverBufs B, PlanPtrs pr) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SolverState* st = B.st;
+    if (st->done) return;
+    const int64_t blk = blockIdx.x;
+    const bool fma = B.fma;
+    const double2 ma = neg(st->alpha);
+    auto f = [&](int64_t e, double (&v)[1]) {
+        double2 s = cadd(B.r[e], f1(ma, B.v[e], fma));
+        B.s[e] = s;
+        if (B.jacobi) B.sh[e] = f1(s, __ldg(B.minv + e), fma);
+        v[0] = abs2_np(s);
+    };
+    double* nodes = reinterpret_cast<double*>(smem + 32 * 1024);
+    double out[1];
+    block_reduce<double, 1>(pr, B.n, kBlock, blk, f, nodes, out);
+    if (threadIdx.x == 0) B.partials[blk] = out[0];
+    if (!arrive_last(&st->counter, gridDim.x)) return;
+    double ss;
+    ordered_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), 4096, &ss);
+    if (threadIdx.x != 0) return;
+    st->counter = 0;
+    st->scheck = (__ddiv_rn(__dsqrt_rn(ss), st->b_norm) <= st->tol) ? 1 : 0;
+}
+
+// ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
+__global__ void __launch_bounds__(kThreads) k_x_alpha(SolverBufs B) {
+    SolverState* st = B.st;
+    if (st->done || !st->scheck) return;
+    const double2 a = st->alpha;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride)
+        B.x[i] = cadd(B.x[i], f1(a, B.ph[i], B.fma));
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha_applied = 1;
+}
+
+// ---- true residual ||b + F1(-1, A x)|| / ||b|| (krylov.py:183-186) ----
+// mode 0: on the s-check path (K6x);  mode 1: end of iteration (K61), fused
+// with the next iteration's p update.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) k_true_res(SellView A, SolverBufs B, PlanPtrs pr,
+                                                       cudaGraphConditionalHandle cond, int use_cond) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* stash = reinterpret_cast<double*>(smem);
+    SolverState* st = B.st;
+    if (st->done || (MODE == 0 && !st->scheck)) {
+        if (MODE == 1 && use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+        return;
+    }
+    const int64_t blk = blockIdx.x, base = blk * kBlock;
+    const bool fma = B.fma;
+    const double2 mw = neg(st->omega), beta = st->beta;
+    auto epi = [&](int64_t row, double2 ax) {
+        double2 res = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, fma));
+        stash[row - base] = abs2_np(res);
+        if (MODE == 1) p_update(B, mw, beta, row);
+    };
+    spmv_block(A, B.x, blk, epi);
+    __syncthreads();
+    double* nodes = reinterpret_cast<double*>(smem + kStashBytes);
+    auto f = [&](int64_t e, double (&v)[1]) { v[0] = stash[e - base]; };
+    double out[1];
+    block_reduce<double, 1>(pr, B.n, kBlock, blk, f, nodes, out);
+    if (threadIdx.x == 0) B.partials[blk] = out[0];
+    if (!arrive_last(&st->counter, gridDim.x)) return;
+    double rr;
+    ordered_fold<double>(B.partials, 1, B.nblocks, stash, 4096, &rr);
+    if (threadIdx.x != 0) return;
+    st->counter = 0;
+    const double rel = __ddiv_rn(__dsqrt_rn(rr), st->b_norm);
+    if (MODE == 0) {
+        if (rel <= st->tol) {
+            st->iterations++;
+            B.hist[st->iterations] = rel;
+            st->last_rel = rel;
+            stop(st, ST_CONVERGED, BD_NONE);
+        }
+        return;
+    }
+    st->iterations++;
+    B.hist[st->iterations] = rel;
+    st->last_rel = rel;
+    st->scheck = 0;
+    st->alpha_applied = 0;
+    if (rel <= st->tol) {
+        stop(st, ST_CONVERGED, BD_NONE);
+    } else if (st->iterations >= st->maxit) {
+        stop(st, ST_NOT_CONVERGED, BD_NONE);
+    } else if (small_py(st->rho_old)) {  // next iteration's checks (krylov.py:256-259)
+        stop(st, ST_BREAKDOWN, BD_RHO);
+    } else if (small_py(st->omega)) {
+        stop(st, ST_BREAKDOWN, BD_OMEGA);
+    }
+    if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+}
+
+// ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
+__global__ void __launch_bounds__(kThreads) k_spmv_t(SellView A, SolverBufs B, PlanPtrs pc) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double2* stash = reinterpret_cast<double2*>(smem);
+    SolverState* st = B.st;
+    if (st->done) return;
+    const int64_t blk = blockIdx.x, base = blk * kBlock;
+    const bool fma = B.fma;
+    auto epi = [&](int64_t row, double2 at) {
+        B.t[row] = at;
+        stash[row - base] = at;
+    };
+    spmv_block(A, B.sh, blk, epi);
+    __syncthreads();
+    double2* nodes = reinterpret_cast<double2*>(smem + kStashBytes);
+    auto f = [&](int64_t e, double2 (&v)[2]) {
+        double2 t = stash[e - base];
+        double2 ct = conjz(t);
+        v[0] = f1(ct, t, fma);
+        v[1] = f1(ct, B.s[e], fma);
+    };
+    double2 out[2];
+    block_reduce<double2, 2>(pc, B.n, kBlock, blk, f, nodes, out);
+    double2* PC = reinterpret_cast<double2*>(B.partials);
+    if (threadIdx.x == 0) {
+        PC[2 * blk] = out[0];
+        PC[2 * blk + 1] = out[1];
+    }
+    if (!arrive_last(&st->counter, gridDim.x)) return;
+    double2 tot[2];
+    ordered_fold<double2>(PC, 2, B.nblocks, stash, 2048, tot);
+    if (threadIdx.x != 0) return;
+    st->counter = 0;
+    if (small_py(tot[0])) {
+        stop(st, ST_BREAKDOWN, BD_TT);
+        return;
+    }
+    const double2 w = cdiv_py(tot[1], tot[0]);
+    st->omega = w;
+    if (small_py(w)) stop(st, ST_BREAKDOWN, BD_OMEGA);
+}
+
+// ---- K5: x, r updates and <r~, r> -> rho', beta (krylov.py:288-290, 255-261) ----
+__global__ void __launch_bounds__(kThreads) k_xr_update(SolverBufs B, PlanPtrs pc) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SolverState* st = B.st;
+    if (st->done) return;
+    const int64_t blk = blockIdx.x;
+    const bool fma = B.fma;
+    const double2 a = st->alpha, w = st->omega, mw = neg(w);
+    const bool applied = st->alpha_applied != 0;
+    auto f = [&](int64_t e, double2 (&v)[1]) {
+        double2 xv = B.x[e];
+        if (!applied) xv = cadd(xv, f1(a, B.ph[e], fma));
+        xv = cadd(xv, f1(w, B.sh[e], fma));
+        B.x[e] = xv;
+        double2 rv = cadd(B.s[e], f1(mw, B.t[e], fma));
+        B.r[e] = rv;
+        v[0] = f1(conjz(__ldg(B.rs + e)), rv, fma);
+    };
+    double2* nodes = reinterpret_cast<double2*>(smem + 32 * 1024);
+    double2 out[1];
+    block_reduce<double2, 1>(pc, B.n, kBlock, blk, f, nodes, out);
+    double2* PC = reinterpret_cast<double2*>(B.partials);
+    if (threadIdx.x == 0) PC[blk] = out[0];
+    if (!arrive_last(&st->counter, gridDim.x)) return;
+    double2 rho_next;
+    ordered_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), 2048, &rho_next);
+    if (threadIdx.x != 0) return;
+    st->counter = 0;
+    const double2 rho = st->rho;
+    st->rho_old = rho;
+    st->rho = rho_next;
+    // beta for the next iteration (speculative: K61 stops before it is used
+    // if the loop ends, and breaks down on the same checks as krylov.py:256-259)
+    if (!small_py(rho) && !small_py(w)) st->beta = cmul_py(cdiv_py(rho_next, rho), cdiv_py(a, w));
+}
+
+}  // namespace
+
+namespace {
+
+template <class K>
+void smem_attr(K kernel, int bytes) {
+    ZK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+struct Launch {
+    zk_context* c;
+    SolverPlan* P;
+    SellView A;
+    PlanPtrs pc, pr;
+    unsigned nb, ew;
+};
+
+void launch_prologue(const Launch& L, cudaStream_t s) {
+    k_setup<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc, L.pr);
+    k_p_first<<<L.ew, kThreads, 0, s>>>(L.P->bufs);
+}
+
+void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond) {
+    k_spmv_pivot<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc);
+    k_s_update<<<L.nb, kThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
+    k_x_alpha<<<L.ew, kThreads, 0, s>>>(L.P->bufs);
+    k_true_res<0><<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pr, cond, 0);
+    k_spmv_t<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc);
+    k_xr_update<<<L.nb, kThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
+    k_true_res<1><<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pr, cond, use_cond);
+}
+constexpr int kBodyKernels = 7;
+
+bool g_attrs_done = false;
+void set_attrs() {
+    if (g_attrs_done) return;
+    smem_attr(k_setup, kSpmvSmem);
+    smem_attr(k_spmv_pivot, kSpmvSmem);
+    smem_attr(k_true_res<0>, kSpmvSmem);
+    smem_attr(k_true_res<1>, kSpmvSmem);
+    smem_attr(k_spmv_t, kSpmvSmem);
+    smem_attr(k_s_update, kEwSmem);
+    smem_attr(k_xr_update, kEwSmem);
+    g_attrs_done = true;
+}
+
+bool use_graph() {
+    const char* e = std::getenv("ZK_SOLVER_LOOP");
+    return !(e && std::strcmp(e, "host") == 0);
+}
+
+void build_graph(const Launch& L) {
+    SolverPlan* P = L.P;
+    cudaStream_t s = L.c->stream;
+    cudaGraph_t g;
+    ZK_CUDA(cudaGraphCreate(&g, 0));
+    // prologue captured into its own graph, embedded as a child node
+    cudaGraph_t gp;
+    ZK_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    launch_prologue(L, s);
+    ZK_CUDA(cudaStreamEndCapture(s, &gp));
+    cudaGraphNode_t npro;
+    ZK_CUDA(cudaGraphAddChildGraphNode(&npro, g, nullptr, 0, gp));
+    ZK_CUDA(cudaGraphDestroy(gp));
+    cudaGraphConditionalHandle cond;
+    ZK_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t nloop;
+    ZK_CUDA(cudaGraphAddNode(&nloop, g, &npro, 1, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    ZK_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    launch_body(L, s, cond, 1);
+    cudaGraph_t body_out;
+    ZK_CUDA(cudaStreamEndCapture(s, &body_out));
+    ZK_CUDA(cudaGraphInstantiate(&P->exec, g, 0));
+    P->graph = g;
+    P->graph_ok = true;
+}
+
+}  // namespace
+
+void destroy_solver_plan(zk_context* c, SolverPlan* P) {
+    if (!P) return;
+    if (P->exec) cudaGraphExecDestroy(P->exec);
+    if (P->graph) cudaGraphDestroy(P->graph);
+    SolverBufs& B = P->bufs;
+    void* ptrs[] = {B.x, B.b, B.minv, B.r, B.rs, B.p, B.v, B.s, B.t, B.partials, B.hist, B.st};
+    for (void* p : ptrs)
+        if (p) c->alloc.free(p);
+    if (B.jacobi) {
+        c->alloc.free(B.ph);
+        c->alloc.free(B.sh);
+    }
+    delete P;
+}
+
+static SolverPlan* get_plan(zk_context* c, zk_csr* A, bool jacobi, int64_t maxit) {
+    SolverPlan*& slot = A->solver[jacobi ? 1 : 0];
+    if (slot && slot->hist_cap < maxit + 1) {
+        destroy_solver_plan(c, slot);
+        slot = nullptr;
+    }
+    if (slot) return slot;
+    SolverPlan* P = new SolverPlan();
+    const int64_t n = A->n_rows;
+    P->n = n;
+    P->jacobi = jacobi;
+    P->hist_cap = maxit + 1 > 1024 ? maxit + 1 : 1024;
+    SolverBufs& B = P->bufs;
+    const size_t vb = sizeof(double2) * (size_t)(n ? n : 1);
+    auto vec = [&]() { return static_cast<double2*>(c->alloc.alloc(vb)); };
+    B.n = n;
+    B.nblocks = (n + kBlock - 1) / kBlock;
+    B.jacobi = jacobi;
+    B.fma = c->fma != 0;
+    B.x = vec(); B.b = vec(); B.r = vec(); B.rs = vec(); B.p = vec(); B.v = vec(); B.s = vec(); B.t = vec();
+    B.minv = jacobi ? vec() : nullptr;
+    B.ph = jacobi ? vec() : B.p;   // identity: M.apply is a copy, bitwise equal
+    B.sh = jacobi ? vec() : B.s;
+    B.partials = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)(B.nblocks ? B.nblocks : 1)));
+    B.hist = static_cast<double*>(c->alloc.alloc(sizeof(double) * P->hist_cap));
+    B.st = static_cast<SolverState*>(c->alloc.alloc(sizeof(SolverState)));
+    slot = P;
+    return P;
+}
+
+// Runs the solve; x_out/history_host/report filled.  Returns ZK_OK or
+// ZK_ERR_BREAKDOWN.
+int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
+                    int64_t maxit, double2* x_out, double* history_host, zk_solve_report* rep) {
+    const int64_t n = A->n_rows;
+    set_attrs();
+    SolverPlan* P = get_plan(c, A, minv != nullptr, maxit);
+    SolverBufs& B = P->bufs;
+    if (B.fma != (c->fma != 0)) {  // fingerprint changed since the graph was built
+        B.fma = c->fma != 0;
+        if (P->exec) cudaGraphExecDestroy(P->exec);
+        if (P->graph) cudaGraphDestroy(P->graph);
+        P->exec = nullptr;
+        P->graph = nullptr;
+        P->graph_ok = false;
+    }
+    cudaStream_t s = c->stream;
+    const size_t vb = sizeof(double2) * (size_t)n;
+    ZK_CUDA(cudaMemcpyAsync(B.b, b, vb, cudaMemcpyDeviceToDevice, s));
+    if (minv) ZK_CUDA(cudaMemcpyAsync(B.minv, minv, vb, cudaMemcpyDeviceToDevice, s));
+    if (x0) ZK_CUDA(cudaMemcpyAsync(B.x, x0, vb, cudaMemcpyDeviceToDevice, s));
+    else ZK_CUDA(cudaMemsetAsync(B.x, 0, vb, s));
+    ZK_CUDA(cudaMemsetAsync(B.p, 0, vb, s));
+    ZK_CUDA(cudaMemsetAsync(B.v, 0, vb, s));
+    SolverState h;
+    std::memset(&h, 0, sizeof(h));
+    h.tol = tol;
+    h.maxit = maxit;
+    ZK_CUDA(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+
+    Launch L{c, P, sell_view(A, c), c->plans_for(n, kBlock, kComplex), c->plans_for(n, kBlock, kReal),
+             (unsigned)B.nblocks, 0};
+    int64_t ewg = (n + kThreads - 1) / kThreads;
+    int64_t cap = (int64_t)num_sms() * 8;
+    L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
+    SolverState out;
+    if (use_graph()) {
+        if (!P->graph_ok) build_graph(L);
+        ZK_CUDA(cudaGraphLaunch(P->exec, s));
+        ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
+        ZK_CUDA(cudaStreamSynchronize(s));
+    } else {
+        launch_prologue(L, s);
+        ZK_CUDA(cudaGetLastError());
+        for (;;) {
+            launch_body(L, s, 0, 0);
+            ZK_CUDA(cudaGetLastError());
+            ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
+            ZK_CUDA(cudaStreamSynchronize(s));
+            if (out.done) break;
+        }
+    }
+    c->launches += 2 + kBodyKernels * out.trips;
+    const int64_t it = out.iterations;
+    ZK_CUDA(cudaMemcpyAsync(history_host, B.hist, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost, s));
+    if (out.trivial_zero) ZK_CUDA(cudaMemsetAsync(x_out, 0, vb, s));
+    else ZK_CUDA(cudaMemcpyAsync(x_out, B.x, vb, cudaMemcpyDeviceToDevice, s));
+    ZK_CUDA(cudaStreamSynchronize(s));
+    rep->iterations = it;
+    rep->converged = out.status == ST_CONVERGED;
+    rep->breakdown = out.status == ST_BREAKDOWN ? out.what : 0;
+    rep->final_relative_residual = history_host[it];
+    rep->history_len = it + 1;
+    rep->kernel_launches = 2 + kBodyKernels * out.trips;
+    return out.status == ST_BREAKDOWN ? ZK_ERR_BREAKDOWN : ZK_OK;
+}
+
+}  // namespace zk

@@ -1,0 +1,200 @@
+// zk_blas1.cu -- level-1 kernels (vecops.py:117-200) for sm_100a.
+//
+// Elementwise kernels are HBM-bound streams: grid-stride over double2
+// (16-byte, coalesced) with 4 independent elements per thread in flight.
+// Reductions run one CTA per ReductionPlan block (zk_reduce.cuh) with the
+// ordered fold done by the last CTA, so a zdot is a single kernel launch.
+#include "zk_internal.h"
+
+namespace zk {
+
+namespace {
+
+constexpr int kEwThreads = 256;
+constexpr int kEwUnroll = 4;
+
+inline int ew_grid(int64_t n) {
+    int64_t per = (int64_t)kEwThreads * kEwUnroll;
+    int64_t g = (n + per - 1) / per;
+    int64_t cap = (int64_t)num_sms() * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+template <class F>
+__device__ __forceinline__ void ew_loop(int64_t n, F f) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + (kEwUnroll - 1) * stride < n; i += kEwUnroll * stride) {
+#pragma unroll
+        for (int u = 0; u < kEwUnroll; ++u) f(i + u * stride);
+    }
+    for (; i < n; i += stride) f(i);
+}
+
+__global__ void k_zscal(int64_t n, double2 a, double2* __restrict__ x, bool fma) {
+    ew_loop(n, [&](int64_t i) { x[i] = f1(x[i], a, fma); });
+}
+
+__global__ void k_zaxpy(int64_t n, double2 a, const double2* __restrict__ x, double2* __restrict__ y, bool fma) {
+    ew_loop(n, [&](int64_t i) { y[i] = cadd(y[i], f1(a, ldg2(x + i), fma)); });
+}
+
+__global__ void k_zaxmy(int64_t n, const double2* __restrict__ x, double2* __restrict__ y, bool fma) {
+    ew_loop(n, [&](int64_t i) { y[i] = f1(y[i], ldg2(x + i), fma); });
+}
+
+__global__ void k_jacobi(int64_t n, const double2* __restrict__ v, const double2* __restrict__ m,
+                         double2* __restrict__ out, bool fma) {
+    ew_loop(n, [&](int64_t i) { out[i] = f1(ldg2(v + i), ldg2(m + i), fma); });
+}
+
+// Blocked zdot: one CTA per block; last CTA folds the partials.
+__global__ void __launch_bounds__(kThreads) k_zdot_blocked(int64_t n, const double2* __restrict__ x,
+                                                           const double2* __restrict__ y, bool conj,
+                                                           int64_t block, PlanPtrs plans, double2* partials,
+                                                           unsigned int* counter, double2* result, bool fma) {
+    extern __shared__ double2 smem_c[];
+    auto f = [&](int64_t e, double2 (&v)[1]) {
+        double2 a = ldg2(x + e);
+        if (conj) a.y = -a.y;
+        v[0] = f1(a, ldg2(y + e), fma);
+    };
+    double2 out[1];
+    block_reduce<double2, 1>(plans, n, block, blockIdx.x, f, smem_c, out);
+    if (threadIdx.x == 0) partials[blockIdx.x] = out[0];
+    if (arrive_last(counter, gridDim.x)) {
+        double2 tot;
+        ordered_fold<double2>(partials, 1, gridDim.x, smem_c, 2048, &tot);
+        if (threadIdx.x == 0) {
+            *result = tot;
+            *counter = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_znorm2_blocked(int64_t n, const double2* __restrict__ x,
+                                                             int64_t block, PlanPtrs plans, double* partials,
+                                                             unsigned int* counter, double* result) {
+    extern __shared__ double smem_r[];
+    auto f = [&](int64_t e, double (&v)[1]) { v[0] = abs2_np(ldg2(x + e)); };
+    double out[1];
+    block_reduce<double, 1>(plans, n, block, blockIdx.x, f, smem_r, out);
+    if (threadIdx.x == 0) partials[blockIdx.x] = out[0];
+    if (arrive_last(counter, gridDim.x)) {
+        double tot;
+        ordered_fold<double>(partials, 1, gridDim.x, smem_r, 4096, &tot);
+        if (threadIdx.x == 0) {
+            *result = __dsqrt_rn(tot);
+            *counter = 0;
+        }
+    }
+}
+
+// SEQUENTIAL plan (vecops.py:175-183): a CPython left-to-right loop with the
+// plain (non-FMA) complex product, starting from 0j.  Correctness path only.
+__global__ void k_zdot_seq(int64_t n, const double2* __restrict__ x, const double2* __restrict__ y, bool conj,
+                           double2* result) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        double2 a = x[i];
+        if (conj) a.y = -a.y;
+        acc = cadd(acc, cmul_py(a, y[i]));
+    }
+    *result = acc;
+}
+
+// vecops.py:194-198: acc += re*re + im*im (Python floats), then math.sqrt.
+__global__ void k_znorm2_seq(int64_t n, const double2* __restrict__ x, double* result) {
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, abs2_np(x[i]));
+    *result = __dsqrt_rn(acc);
+}
+
+}  // namespace
+
+// Shared-memory bytes for the block pass + fold of a plan pair.
+size_t reduce_smem_bytes(int nnodes, int nacc, size_t vbytes, int64_t fold_chunk) {
+    size_t a = (size_t)nnodes * nacc * vbytes;
+    size_t b = (size_t)fold_chunk * nacc * vbytes;
+    return a > b ? a : b;
+}
+
+void launch_zscal(zk_context* c, int64_t n, double2 a, double2* x) {
+    if (n <= 0) return;
+    k_zscal<<<ew_grid(n), kEwThreads, 0, c->stream>>>(n, a, x, c->fma);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+void launch_zaxpy(zk_context* c, int64_t n, double2 a, const double2* x, double2* y) {
+    if (n <= 0) return;
+    k_zaxpy<<<ew_grid(n), kEwThreads, 0, c->stream>>>(n, a, x, y, c->fma);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+void launch_zaxmy(zk_context* c, int64_t n, const double2* x, double2* y) {
+    if (n <= 0) return;
+    k_zaxmy<<<ew_grid(n), kEwThreads, 0, c->stream>>>(n, x, y, c->fma);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+void launch_jacobi(zk_context* c, int64_t n, const double2* v, const double2* m, double2* out) {
+    if (n <= 0) return;
+    k_jacobi<<<ew_grid(n), kEwThreads, 0, c->stream>>>(n, v, m, out, c->fma);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+int plan_nnodes(zk_context* c, int32_t L, int32_t kind);
+
+void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, bool conj, int64_t block,
+                 int mode, double2* result) {
+    if (mode == ZK_MODE_SEQUENTIAL) {
+        k_zdot_seq<<<1, 1, 0, c->stream>>>(n, x, y, conj, result);
+        ZK_CUDA(cudaGetLastError());
+        c->launches++;
+        return;
+    }
+    int64_t nb = (n + block - 1) / block;
+    PlanPtrs p = c->plans_for(n, block, kComplex);
+    int nnodes = plan_nnodes(c, (int32_t)(block - 1), kComplex);
+    int tail = (int32_t)(n - (nb - 1) * block) - 1;
+    int nn2 = plan_nnodes(c, tail, kComplex);
+    if (nn2 > nnodes) nnodes = nn2;
+    size_t smem = reduce_smem_bytes(nnodes, 1, sizeof(double2), 2048);
+    double2* partials = static_cast<double2*>(c->scratch_partials(sizeof(double2) * nb));
+    if (smem > 48 * 1024)
+        ZK_CUDA(cudaFuncSetAttribute(k_zdot_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_zdot_blocked<<<(unsigned)nb, kThreads, smem, c->stream>>>(n, x, y, conj, block, p, partials, c->counter,
+                                                                 result, c->fma);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result) {
+    if (mode == ZK_MODE_SEQUENTIAL) {
+        k_znorm2_seq<<<1, 1, 0, c->stream>>>(n, x, result);
+        ZK_CUDA(cudaGetLastError());
+        c->launches++;
+        return;
+    }
+    int64_t nb = (n + block - 1) / block;
+    PlanPtrs p = c->plans_for(n, block, kReal);
+    int nnodes = plan_nnodes(c, (int32_t)(block - 1), kReal);
+    int tail = (int32_t)(n - (nb - 1) * block) - 1;
+    int nn2 = plan_nnodes(c, tail, kReal);
+    if (nn2 > nnodes) nnodes = nn2;
+    size_t smem = reduce_smem_bytes(nnodes, 1, sizeof(double), 4096);
+    double* partials = static_cast<double*>(c->scratch_partials(sizeof(double) * nb));
+    if (smem > 48 * 1024)
+        ZK_CUDA(cudaFuncSetAttribute(k_znorm2_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_znorm2_blocked<<<(unsigned)nb, kThreads, smem, c->stream>>>(n, x, block, p, partials, c->counter, result);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+}  // namespace zk

@@ -1,0 +1,99 @@
+// zk_internal.h -- host-side objects behind the C ABI (include/zk.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/zk.h"
+#include "zk_plan.h"
+#include "zk_reduce.cuh"
+
+namespace zk {
+
+void set_error(const std::string& msg);
+
+struct CudaError {
+    cudaError_t err;
+    std::string where;
+};
+
+#define ZK_CUDA(call)                                                             \
+    do {                                                                          \
+        cudaError_t _e = (call);                                                  \
+        if (_e != cudaSuccess) throw ::zk::CudaError{_e, #call};                  \
+    } while (0)
+
+struct ZkError {
+    int code;
+    std::string msg;
+};
+
+// Size-class caching allocator over cudaMalloc (cudaFree synchronises the
+// device, and the reference test-suite creates thousands of small vectors).
+class Allocator {
+public:
+    void* alloc(size_t bytes);
+    void free(void* p);
+    void release_cached();
+    size_t bytes_in_use() const { return in_use_; }
+    ~Allocator();
+
+private:
+    static size_t round(size_t b);
+    std::map<size_t, std::vector<void*>> cache_;
+    std::map<void*, size_t> live_;
+    size_t in_use_ = 0;
+};
+
+struct SolverPlan;  // zk_bicgstab.cu
+
+}  // namespace zk
+
+// SELL-32 device matrix (see zk_spmv.cu for the layout).
+struct zk_csr {
+    zk_context* ctx;
+    int64_t n_rows, n_cols, nnz;
+    int64_t nslices, nblocks;       // 32-row slices, 4096-row blocks
+    int64_t sell_elems;             // padded element count
+    double2* aa;                    // [sell_elems]
+    int32_t* ja;                    // [sell_elems]
+    int64_t* slice_off;             // [nslices + 1]
+    uint8_t* rowlen;                // [nslices * 32]; 255 = long row
+    int32_t n_long;
+    int32_t* long_row;              // [n_long]
+    int32_t* long_blk_ptr;          // [nblocks + 1]
+    int64_t* long_ia;               // [n_long + 1]
+    int32_t* long_ja;
+    double2* long_aa;
+    zk::SolverPlan* solver[2];      // [identity, jacobi]
+};
+
+struct zk_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    zk::Allocator alloc;
+    std::map<std::pair<int32_t, int32_t>, char*> plans;  // (L, kind) -> device plan
+    int fma = 1;
+    int64_t elide_bytes = 262144;
+    // scratch for API reductions
+    void* partials = nullptr;
+    size_t partials_bytes = 0;
+    unsigned int* counter = nullptr;
+    double* d_result = nullptr;    // 4 doubles
+    double* h_result = nullptr;    // pinned, 4 doubles
+    int64_t launches = 0;          // kernels launched by this context
+    std::mutex mu;
+
+    char* plan(int32_t L, int32_t kind);
+    zk::PlanPtrs plans_for(int64_t n, int64_t block, int32_t kind);
+    void* scratch_partials(size_t bytes);
+};
+
+namespace zk {
+int num_sms();
+}

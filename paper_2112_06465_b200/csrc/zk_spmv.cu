@@ -1,0 +1,165 @@
+// zk_spmv.cu -- CSR -> SELL-32 conversion and the plain SpMV kernel.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "zk_internal.h"
+#include "zk_spmv.cuh"
+
+namespace zk {
+
+SellView sell_view(const zk_csr* A, const zk_context* c) {
+    SellView v;
+    v.n_rows = A->n_rows;
+    v.n_cols = A->n_cols;
+    v.nslices = A->nslices;
+    v.nblocks = A->nblocks;
+    v.aa = A->aa;
+    v.ja = A->ja;
+    v.slice_off = A->slice_off;
+    v.rowlen = A->rowlen;
+    v.long_row = A->long_row;
+    v.long_blk_ptr = A->n_long ? A->long_blk_ptr : nullptr;
+    v.long_ia = A->long_ia;
+    v.long_ja = A->long_ja;
+    v.long_aa = A->long_aa;
+    v.swap = (A->nnz * 16 >= c->elide_bytes);
+    v.fma = c->fma != 0;
+    return v;
+}
+
+namespace {
+
+// Scatter CSR rows into the SELL layout (thread per short row) and the side
+// CSR (thread per long row).  Setup only.
+__global__ void k_sell_scatter(int64_t n_rows, const int64_t* __restrict__ ia, const int64_t* __restrict__ ja,
+                               const double2* __restrict__ aa, const int64_t* __restrict__ slice_off,
+                               const uint8_t* __restrict__ rowlen, double2* __restrict__ saa,
+                               int32_t* __restrict__ sja) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n_rows) return;
+    const int len = rowlen[row];
+    if (len == 255) return;
+    const int64_t base = slice_off[row / kSlice] + (row % kSlice);
+    const int64_t lo = ia[row];
+    for (int k = 0; k < len; ++k) {
+        saa[base + 32 * (int64_t)k] = aa[lo + k];
+        sja[base + 32 * (int64_t)k] = (int32_t)ja[lo + k];
+    }
+}
+
+__global__ void k_long_scatter(int32_t n_long, const int32_t* __restrict__ long_row, const int64_t* __restrict__ ia,
+                               const int64_t* __restrict__ ja, const double2* __restrict__ aa,
+                               const int64_t* __restrict__ long_ia, int32_t* __restrict__ lja,
+                               double2* __restrict__ laa) {
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= n_long) return;
+    const int64_t lo = ia[long_row[li]], len = long_ia[li + 1] - long_ia[li];
+    for (int64_t k = 0; k < len; ++k) {
+        lja[long_ia[li] + k] = (int32_t)ja[lo + k];
+        laa[long_ia[li] + k] = aa[lo + k];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_spmv(SellView A, const double2* __restrict__ x, double2* __restrict__ y) {
+    auto epi = [&](int64_t row, double2 v) { y[row] = v; };
+    spmv_block(A, x, blockIdx.x, epi);
+}
+
+template <class T>
+T* dalloc(zk_context* c, size_t count) {
+    return static_cast<T*>(c->alloc.alloc(sizeof(T) * (count ? count : 1)));
+}
+
+}  // namespace
+
+// Builds the SELL matrix from device CSR arrays and the host copy of ia.
+zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
+                   const int64_t* ia_d, const int64_t* ja_d, const double2* aa_d) {
+    zk_csr* A = new zk_csr();
+    std::memset(A, 0, sizeof(*A));
+    A->ctx = c;
+    A->n_rows = n_rows;
+    A->n_cols = n_cols;
+    A->nnz = nnz;
+    A->nslices = (n_rows + kSlice - 1) / kSlice;
+    A->nblocks = (n_rows + kBlock - 1) / kBlock;
+    const int64_t nrp = A->nslices * kSlice;
+    std::vector<uint8_t> rowlen(nrp, 0);
+    std::vector<int64_t> slice_off(A->nslices + 1, 0);
+    std::vector<int32_t> long_row;
+    std::vector<int32_t> long_blk_ptr(A->nblocks + 1, 0);
+    std::vector<int64_t> long_ia(1, 0);
+    for (int64_t s = 0; s < A->nslices; ++s) {
+        int w = 0;
+        for (int r = 0; r < kSlice; ++r) {
+            const int64_t row = s * kSlice + r;
+            if (row >= n_rows) break;
+            const int64_t len = ia_h[row + 1] - ia_h[row];
+            if (len > kShortMax) {
+                rowlen[row] = 255;
+                long_row.push_back((int32_t)row);
+                long_ia.push_back(long_ia.back() + len);
+                long_blk_ptr[row / kBlock + 1]++;
+            } else {
+                rowlen[row] = (uint8_t)len;
+                w = std::max(w, (int)len);
+            }
+        }
+        slice_off[s + 1] = slice_off[s] + (int64_t)kSlice * w;
+    }
+    for (int64_t b = 0; b < A->nblocks; ++b) long_blk_ptr[b + 1] += long_blk_ptr[b];
+    A->sell_elems = slice_off[A->nslices];
+    A->n_long = (int32_t)long_row.size();
+    cudaStream_t st = c->stream;
+    A->aa = dalloc<double2>(c, A->sell_elems);
+    A->ja = dalloc<int32_t>(c, A->sell_elems);
+    A->slice_off = dalloc<int64_t>(c, A->nslices + 1);
+    A->rowlen = dalloc<uint8_t>(c, nrp);
+    ZK_CUDA(cudaMemsetAsync(A->aa, 0, sizeof(double2) * A->sell_elems, st));
+    ZK_CUDA(cudaMemsetAsync(A->ja, 0, sizeof(int32_t) * A->sell_elems, st));
+    ZK_CUDA(cudaMemcpyAsync(A->slice_off, slice_off.data(), sizeof(int64_t) * slice_off.size(),
+                            cudaMemcpyHostToDevice, st));
+    ZK_CUDA(cudaMemcpyAsync(A->rowlen, rowlen.data(), nrp, cudaMemcpyHostToDevice, st));
+    if (n_rows > 0) {
+        k_sell_scatter<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(n_rows, ia_d, ja_d, aa_d, A->slice_off,
+                                                                         A->rowlen, A->aa, A->ja);
+        ZK_CUDA(cudaGetLastError());
+        c->launches++;
+    }
+    if (A->n_long) {
+        A->long_row = dalloc<int32_t>(c, A->n_long);
+        A->long_blk_ptr = dalloc<int32_t>(c, A->nblocks + 1);
+        A->long_ia = dalloc<int64_t>(c, A->n_long + 1);
+        A->long_ja = dalloc<int32_t>(c, long_ia.back());
+        A->long_aa = dalloc<double2>(c, long_ia.back());
+        ZK_CUDA(cudaMemcpyAsync(A->long_row, long_row.data(), sizeof(int32_t) * A->n_long, cudaMemcpyHostToDevice, st));
+        ZK_CUDA(cudaMemcpyAsync(A->long_blk_ptr, long_blk_ptr.data(), sizeof(int32_t) * long_blk_ptr.size(),
+                                cudaMemcpyHostToDevice, st));
+        ZK_CUDA(cudaMemcpyAsync(A->long_ia, long_ia.data(), sizeof(int64_t) * long_ia.size(), cudaMemcpyHostToDevice,
+                                st));
+        k_long_scatter<<<(A->n_long + 255) / 256, 256, 0, st>>>(A->n_long, A->long_row, ia_d, ja_d, aa_d, A->long_ia,
+                                                               A->long_ja, A->long_aa);
+        ZK_CUDA(cudaGetLastError());
+        c->launches++;
+    }
+    // host vectors are freed on return: wait for the async copies
+    ZK_CUDA(cudaStreamSynchronize(st));
+    return A;
+}
+
+void destroy_sell(zk_csr* A);
+
+void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
+    if (A->n_rows == 0) return;
+    if (A->nnz == 0) {
+        ZK_CUDA(cudaMemsetAsync(y, 0, sizeof(double2) * A->n_rows, c->stream));
+        return;
+    }
+    SellView v = sell_view(A, c);
+    k_spmv<<<(unsigned)A->nblocks, kThreads, 0, c->stream>>>(v, x, y);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+}  // namespace zk

@@ -1,0 +1,164 @@
+"""Right-preconditioned BiCGStab on the device (drop-in for the hot-path part
+of zlinalg krylov.py).
+
+``solve_bicgstab`` hands the whole loop to libzk (``zk_bicgstab``,
+csrc/zk_bicgstab.cu): every vector stays in HBM, axpy/scale updates are fused
+with the reductions that follow them, the scalar recurrences run on the
+device in Python's arithmetic, and the host waits once for the final report.
+Results (solution, iteration count, every residual-history entry) are the
+reference's bit for bit (krylov.py:213-295).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import BreakdownError, DimensionError, ParameterError, SingularPreconditionerError
+from .sparse import CsrMatrix
+from .vecops import ZVector
+
+__all__ = ["SolverConfig", "Preconditioner", "SolveReport", "build_jacobi", "solve_bicgstab"]
+
+_BREAKDOWN_EPS = 1e-300
+_BREAKDOWN_WHAT = {
+    1: "rho",
+    2: "omega",
+    3: "shadow pivot <r~, A M^-1 p>",
+    4: "omega denominator <t, t>",
+}
+
+
+@dataclass(frozen=True)
+class SolverConfig:
+    """Tolerance, iteration cap and optional initial guess (krylov.py:51-72)."""
+
+    tolerance: float = 1e-9
+    max_iterations: int = 1000
+    initial_guess: ZVector | None = None
+    l: int = 8
+
+    def __post_init__(self):
+        if not self.tolerance > 0:
+            raise ParameterError(f"tolerance must be positive, got {self.tolerance!r}")
+        if self.max_iterations < 1:
+            raise ParameterError(f"max_iterations must be >= 1, got {self.max_iterations!r}")
+        if self.l < 1:
+            raise ParameterError(f"polynomial degree l must be >= 1, got {self.l!r}")
+
+
+class Preconditioner:
+    """Right preconditioner: ``identity`` or ``jacobi`` (stored inverse diagonal
+    ``data``, complex128, host array; a device copy is cached on first use)."""
+
+    __slots__ = ("kind", "data", "_dev")
+
+    def __init__(self, kind: str, data: np.ndarray | None = None):
+        if kind not in ("identity", "jacobi"):
+            raise ParameterError(f"unknown preconditioner kind {kind!r}")
+        if kind == "jacobi" and data is None:
+            raise ParameterError("jacobi preconditioner needs the inverse diagonal")
+        self.kind = kind
+        self.data = data
+        self._dev = None
+
+    @classmethod
+    def identity(cls) -> "Preconditioner":
+        return cls("identity")
+
+    def _device_minv(self) -> ZVector:
+        if self._dev is None or self._dev[0] is not self.data:
+            self._dev = (self.data, ZVector(np.asarray(self.data, dtype=np.complex128)))
+        return self._dev[1]
+
+    def apply(self, v: ZVector) -> ZVector:
+        """M^-1 v as a new vector (krylov.py:92-100)."""
+        if self.kind == "identity":
+            return v.copy()
+        if self.data.shape[0] != len(v):
+            raise DimensionError(f"preconditioner built for size {self.data.shape[0]}, vector has {len(v)}")
+        out = ZVector._device_new(len(v))
+        if len(v):
+            m = self._device_minv()._dptr()
+            _lib.check(_lib.lib().zk_jacobi_apply(_lib.context(), len(v), v._dptr(), m, out._dptr_out()))
+        return out._written()
+
+    def __repr__(self):
+        return f"Preconditioner({self.kind})"
+
+
+def build_jacobi(A: CsrMatrix) -> Preconditioner:
+    """Inverse main diagonal (krylov.py:106-120).  Host setup: the quotient is
+    numpy's own complex division, exactly as the reference forms it."""
+    diag = A.diagonal()
+    zero = np.flatnonzero(diag == 0)
+    if zero.size:
+        raise SingularPreconditionerError(
+            f"zero diagonal entry at row {int(zero[0])}; Jacobi preconditioner is singular")
+    return Preconditioner("jacobi", np.divide(1.0, diag))
+
+
+@dataclass
+class SolveReport:
+    """Per-solve bookkeeping (krylov.py:123-136)."""
+
+    iterations: int = 0
+    final_relative_residual: float = math.inf
+    converged: bool = False
+    residual_history: list = field(default_factory=list)
+    elapsed_ms: float = 0.0
+
+
+def solve_bicgstab(A, b, M=None, cfg=None):
+    """Right-preconditioned BiCGStab (van der Vorst), device-resident.
+
+    Returns ``(x, SolveReport)``; non-convergence is a normal return.  Raises
+    ``BreakdownError`` (with the partial report) when rho, the shadow pivot,
+    <t,t> or omega falls below 1e-300 in magnitude.
+    """
+    cfg = cfg or SolverConfig()
+    n = A.n
+    if len(b) != n:
+        raise DimensionError(f"matrix is {n}x{n} but right-hand side has {len(b)} elements")
+    M = M if M is not None else Preconditioner.identity()
+    if M.kind == "jacobi" and M.data.shape[0] != n:
+        raise DimensionError(f"preconditioner built for size {M.data.shape[0]}, matrix is {n}x{n}")
+    t0 = time.perf_counter()
+    guess = cfg.initial_guess
+    if guess is not None and len(guess) != n:
+        raise DimensionError(f"initial guess has {len(guess)} elements, need {n}")
+    maxit = int(cfg.max_iterations)
+    hist = (ctypes.c_double * (maxit + 1))()
+    rep = _lib.SolveReportC()
+    x = ZVector._device_new(n)
+    if n:
+        bp = b._dptr()
+        mp = M._device_minv()._dptr() if M.kind == "jacobi" else None
+        gp = guess._dptr() if guess is not None else None
+        status = _lib.lib().zk_bicgstab(_lib.context(), A._device(), bp, mp, gp, float(cfg.tolerance), maxit,
+                                        x._dptr_out(), hist, ctypes.byref(rep))
+    else:
+        status = _lib.lib().zk_bicgstab(_lib.context(), A._device(), None, None, None, float(cfg.tolerance),
+                                        maxit, None, hist, ctypes.byref(rep))
+    if status not in (_lib.ZK_OK, _lib.ZK_ERR_BREAKDOWN):
+        _lib.check(status)
+    x._written()
+    history = list(hist[: rep.history_len])
+    report = SolveReport(
+        iterations=int(rep.iterations),
+        final_relative_residual=history[-1],
+        converged=bool(rep.converged),
+        residual_history=history,
+        elapsed_ms=(time.perf_counter() - t0) * 1e3,
+    )
+    report.kernel_launches = int(rep.kernel_launches)  # extra attribute, not in the reference
+    if status == _lib.ZK_ERR_BREAKDOWN:
+        what = _BREAKDOWN_WHAT.get(int(rep.breakdown), "recurrence")
+        raise BreakdownError(
+            f"{what} numerically zero (|value| < {_BREAKDOWN_EPS:g}) after {report.iterations} iterations",
+            report=report)
+    return x, report

@@ -1,0 +1,155 @@
+"""Bitwise parity of the CUDA path with the reference (golden vectors made
+by the live reference) and with the C oracle (larger seeded inputs).
+
+Everything here calls the product through its public API, which goes
+through the C ABI of libzk.so.  Comparisons are on raw bytes: SpMV, level-1
+and BiCGStab results must be the reference's bits, not merely close.
+"""
+import numpy as np
+import pytest
+
+import paper_2112_06465_b200 as Z
+from oracle import oracle as O
+from paper_2112_06465_b200 import problems
+from helpers import bits
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _arith():
+    Z.set_arithmetic(True, 262144)
+    O.set_arith(True, 262144)
+
+
+# ---- level 1 vs golden ---------------------------------------------------------
+
+def test_vecops_golden(vecops_golden):
+    for case, g in vecops_golden.items():
+        X, Y = Z.ZVector(g["x"].copy()), Z.ZVector(g["y"].copy())
+        for conj, tag in ((True, "c"), (False, "u")):
+            for bs in (64, 4096, 65536):
+                got = complex(Z.zdot(X, Y, conj, Z.ReductionPlan(bs)))
+                assert bits([got]) == bits(g[f"dot_{tag}_{bs}"]), (case, tag, bs)
+            if f"dot_{tag}_seq" in g:
+                got = complex(Z.zdot(X, Y, conj, Z.ReductionPlan(mode=Z.SEQUENTIAL)))
+                assert bits([got]) == bits(g[f"dot_{tag}_seq"]), (case, tag)
+        for bs in (64, 4096, 65536):
+            assert np.float64(Z.znorm2(X, Z.ReductionPlan(bs))).tobytes() == g[f"norm_{bs}"].tobytes(), (case, bs)
+        if "norm_seq" in g:
+            assert np.float64(Z.znorm2(X, Z.ReductionPlan(mode=Z.SEQUENTIAL))).tobytes() == g["norm_seq"].tobytes()
+        if "axpy" in g:
+            a = complex(g["alpha"][0])
+            assert bits(Z.zaxpy(a, X, Z.ZVector(g["y"].copy())).data) == bits(g["axpy"]), case
+            assert bits(Z.zscal(a, Z.ZVector(g["x"].copy())).data) == bits(g["scal"]), case
+            assert bits(Z.zaxmy(X, Z.ZVector(g["y"].copy())).data) == bits(g["axmy"]), case
+            M = Z.Preconditioner("jacobi", g["minv"])
+            assert bits(M.apply(X).data) == bits(g["jacobi"]), case
+
+
+@pytest.mark.parametrize("n", [1_000_000, 3 * 4096 + 17, 10_000_019])
+def test_zdot_znorm2_vs_oracle_large(n):
+    rng = np.random.default_rng(n)
+    x = rng.random(n) + 1j * rng.random(n)
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    X, Y = Z.ZVector(x), Z.ZVector(y)
+    for conj in (True, False):
+        assert bits([complex(Z.zdot(X, Y, conj))]) == bits([O.zdot(x, y, conj)])
+    assert Z.znorm2(Y) == O.znorm2(y)
+    assert Z.znorm2(X, Z.ReductionPlan(65536)) == O.znorm2(x, 65536)
+
+
+# ---- SpMV ------------------------------------------------------------------------
+
+def test_spmv_golden(spmv_golden):
+    for case, g in spmv_golden.items():
+        nr, nc = (int(v) for v in g["shape"])
+        A = Z.CsrMatrix(nr, nc, g["aa"], g["ja"], g["ia"])
+        y = Z.spmv(A, Z.ZVector(g["x"]))
+        assert bits(y.data) == bits(g["y"]), case
+
+
+@pytest.mark.parametrize("kind", ["fd7_damped", "fd7_undamped", "s27", "ragged"])
+def test_spmv_vs_oracle_large(kind):
+    rng = np.random.default_rng(7)
+    if kind == "fd7_damped":
+        n, ia, ja, aa, _ = problems.helmholtz_fd(3, 65, frequency=5.0, damping=0.3)
+    elif kind == "fd7_undamped":
+        n, ia, ja, aa, _ = problems.helmholtz_fd(3, 41, frequency=2.0)
+    elif kind == "s27":
+        n, ia, ja, aa, _ = problems.helmholtz_27pt(40)
+    else:  # ragged rows incl. empty, short (<5) and long (> 65) rows, random values
+        n = 20000
+        lens = rng.integers(0, 12, n)
+        lens[rng.integers(0, n, 40)] = rng.integers(66, 400, 40)
+        lens[:50] = 0
+        ia = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(lens, out=ia[1:])
+        ja = np.concatenate([np.sort(rng.choice(n, size=int(k), replace=False)) for k in lens]).astype(np.int64)
+        aa = rng.standard_normal(ia[-1]) + 1j * rng.standard_normal(ia[-1])
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y = Z.spmv(A, Z.ZVector(x)).data
+    assert bits(y) == bits(O.spmv(n, n, ia, ja, aa, x))
+
+
+# ---- BiCGStab --------------------------------------------------------------------
+
+def _solve_golden(g):
+    n = g["b"].shape[0]
+    A = Z.CsrMatrix(n, n, g["aa"], g["ja"], g["ia"])
+    M = Z.Preconditioner("jacobi", g["minv"]) if g["minv"].size else Z.Preconditioner.identity()
+    tol, maxit = float(g["params"][0]), int(g["params"][1])
+    guess = Z.ZVector(g["guess"].copy()) if g["guess"].size else None
+    cfg = Z.SolverConfig(tolerance=tol, max_iterations=maxit, initial_guess=guess)
+    return Z.solve_bicgstab(A, Z.ZVector(g["b"].copy()), M, cfg)
+
+
+def test_bicgstab_golden(bicgstab_golden):
+    for case, g in bicgstab_golden.items():
+        status = str(g["status"][0])
+        if status == "breakdown":
+            with pytest.raises(Z.BreakdownError) as info:
+                _solve_golden(g)
+            assert str(info.value) == str(g["what"][0]), case
+            assert np.array(info.value.report.residual_history).tobytes() == g["hist"].tobytes(), case
+            continue
+        x, rep = _solve_golden(g)
+        assert np.array(rep.residual_history).tobytes() == g["hist"].tobytes(), case
+        assert rep.converged == (status == "converged"), case
+        assert rep.iterations == len(g["hist"]) - 1, case
+        assert bits(x.data) == bits(g["x"]), case
+
+
+@pytest.mark.parametrize("shape", [("fd", 49, 49 / 12.0, 0.3), ("s27", 30, 0, 0), ("fd", 65, 3.0, 0.0)])
+def test_bicgstab_vs_oracle_multiblock(shape):
+    """Larger systems (many 4096-row blocks, partial tail block) vs the C oracle."""
+    kind, m, freq, eps = shape
+    if kind == "fd":
+        n, ia, ja, aa, b = problems.helmholtz_fd(3, m, frequency=freq, damping=eps)
+    else:
+        n, ia, ja, aa, b = problems.helmholtz_27pt(m, k2=100.0, damping=0.05)
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    M = Z.build_jacobi(A)
+    x, rep = Z.solve_bicgstab(A, Z.ZVector(b), M, Z.SolverConfig(tolerance=1e-8, max_iterations=3000))
+    xo, hist, it, st, _ = O.bicgstab(n, ia, ja, aa, b, M.data, None, 1e-8, 3000)
+    assert rep.iterations == it
+    assert np.array(rep.residual_history).tobytes() == np.array(hist).tobytes()
+    assert bits(x.data) == bits(xo)
+
+
+def test_solver_host_loop_matches_graph(monkeypatch, bicgstab_golden):
+    """The CUDA-graph WHILE loop and the host-driven loop are the same kernels."""
+    monkeypatch.setenv("ZK_SOLVER_LOOP", "host")
+    g = bicgstab_golden["damped21"]
+    x, rep = _solve_golden(g)
+    assert np.array(rep.residual_history).tobytes() == g["hist"].tobytes()
+    assert bits(x.data) == bits(g["x"])
+
+
+def test_solver_reuse_and_determinism(bicgstab_golden):
+    g = bicgstab_golden["fd13"]
+    r1 = _solve_golden(g)
+    r2 = _solve_golden(g)
+    assert r1[1].residual_history == r2[1].residual_history
+    assert bits(r1[0].data) == bits(r2[0].data)
