@@ -1,0 +1,440 @@
+"""Benchmark: Jacobi-preconditioned BiCGStab solves/sec on BASELINE config C4
+(car-compartment-scale 27-point Helmholtz, 200^3 = 8M rows, 214M nnz), with
+zSpMV / zdotc GB/s against the HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl zk|reference]
+
+One step = one complete solve (b -> x, tol 1e-8) through the product path.
+`value` is timed with CUDA events on the library stream with every input
+resident in HBM; `e2e` repeats the solve through the public Python API with
+the matrix, right-hand side and preconditioner in pinned host memory (the
+device copy of the matrix is dropped before every step, so each step uploads
+and re-lays-out all 5.1 GB) and the solution read back.  The matrix (4.6 GB
+in the device layout) is far larger than the 126 MB L2, so no flush is
+needed between steps.
+
+`--impl reference` times the reference's own CPU algorithm (oracle/port.py,
+the same numpy operations as zlinalg) on this host, one BiCGStab iteration
+per step, and extrapolates solves/sec with the iteration count of the
+configuration (identical on both sides: the GPU path is bitwise the
+reference).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "C4"
+TOL = 1e-8
+MAXIT = 5000
+# Iterations of the C4 solve (bitwise identical between this GPU path and the
+# reference algorithm; the GPU arm re-measures it every run and reports both).
+C4_ITERATIONS_KNOWN = None
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+# ---- distributed plumbing ---------------------------------------------------
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.dist, self.torch = dist, torch
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ---- clocks -------------------------------------------------------------------
+
+class Clocks:
+    """nvidia-smi sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    mx = float(f[1])
+                except ValueError:
+                    continue
+                for name, val in zip(names, f[4:8]):
+                    if val.lower() == "active":
+                        reasons.add(name)
+        finally:
+            os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+# ---- workload -------------------------------------------------------------------
+
+def build_problem(config: str = CONFIG):
+    from paper_2112_06465_b200 import problems
+    n, ia, ja, aa, b = problems.config_problem(config)
+    return n, ia, ja, aa, b
+
+
+def algorithmic_bytes(n: int, nnz: int):
+    """SURVEY 8d byte model (int32-index CSR, every array counted once)."""
+    A = 20 * nnz + 4 * (n + 1) + 16 * n + 16 * n
+    Ar = 20 * nnz + 4 * (n + 1)  # matrix stream only
+    return {
+        "spmv": A,
+        "spmv_pivot": A + 16 * n,             # + r~ read for <r~, v>
+        "spmv_t": A + 16 * n,                 # + s read for <t, s>
+        "true_res_p": Ar + 32 * n + 96 * n,   # A, x, b  + p-update (p, v, r, minv -> p, p^)
+        "true_res_s": Ar + 32 * n,
+        "s_update": 80 * n,
+        "xr_update": 128 * n,
+        "x_alpha": 48 * n,
+        "p_first": 96 * n,
+        "iteration": 3 * A + 336 * n,
+    }
+
+
+def traffic_from_profiles(kernel: str):
+    """dram bytes per launch for `kernel` from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(kernel)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def run_zk(args, dist: Dist):
+    import paper_2112_06465_b200 as Z
+    from paper_2112_06465_b200 import _lib
+
+    peak, peak_kind = peaks()
+    t0 = time.time()
+    n, ia, ja, aa, b = build_problem()
+    nnz = int(ia[-1])
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    M = Z.build_jacobi(A)
+    bv = Z.ZVector(b)
+    cfg = Z.SolverConfig(tolerance=TOL, max_iterations=MAXIT)
+    setup_s = time.time() - t0
+
+    # ---- value: device-resident solves -------------------------------------
+    A._device()
+    bv._dptr()
+    M._device_minv()._dptr()
+    for _ in range(args.warmup):
+        x, rep = Z.solve_bicgstab(A, bv, M, cfg)
+    iters = rep.iterations
+    dist.barrier()
+    _lib.synchronize()
+    l0 = Z.launch_count()
+    with Clocks(dist.local) as clk:
+        _lib.event_record(0)
+        for _ in range(args.steps):
+            x, rep = Z.solve_bicgstab(A, bv, M, cfg)
+        _lib.event_record(1)
+        ms = _lib.event_elapsed_ms(0, 1)
+    launches = Z.launch_count() - l0
+    _lib.synchronize()
+    dist.barrier()
+    ms_max = dist.max(ms)
+    clocks = clk.summary()
+    step_ms = ms_max / args.steps
+    value = dist.world * args.steps / (ms_max / 1e3)  # replicas: every rank solves
+
+    # ---- e2e: public API, pinned host inputs, fresh upload every step ---------
+    pinned = [ia, ja, aa, b, M.data]
+    for arr in pinned:
+        _lib.host_register(arr)
+    e2e_ms = []
+    try:
+        for k in range(args.steps + 1):
+            Ae = Z.CsrMatrix(n, n, aa, ja, ia, validate=False)
+            Me = Z.Preconditioner("jacobi", M.data)
+            be = Z.ZVector(b)
+            dist.barrier()
+            _lib.synchronize()
+            _lib.event_record(2)
+            xe, repe = Z.solve_bicgstab(Ae, be, Me, cfg)
+            xh = xe.data
+            _lib.event_record(3)
+            t = _lib.event_elapsed_ms(2, 3)
+            if k:  # the first call also builds the solver graph; keep it as warm-up
+                e2e_ms.append(t)
+            del Ae
+    finally:
+        for arr in pinned:
+            _lib.host_unregister(arr)
+    e2e_step = dist.max(sum(e2e_ms) / len(e2e_ms))
+    assert repe.iterations == iters and xh.tobytes() == x.data.tobytes()
+    h2d = ia.nbytes + ja.nbytes + aa.nbytes + b.nbytes + M.data.nbytes
+    d2h = 16 * n + 8 * (iters + 1)
+
+    # ---- per-phase kernel times (host loop with events around each kernel) ----
+    _lib.profile_enable(True)
+    Z.solve_bicgstab(A, bv, M, cfg)
+    prof = _lib.profile_read()
+    _lib.profile_enable(False)
+    B = algorithmic_bytes(n, nnz)
+    phases = {}
+    for name, (tms, cnt) in prof.items():
+        if cnt:
+            avg = tms / cnt
+            entry = {"launches": cnt, "avg_us": round(avg * 1e3, 2), "total_ms": round(tms, 3)}
+            if name in B:
+                entry["gbs"] = round(B[name] / (avg * 1e-3) / 1e9, 1)
+            phases[name] = entry
+    body = [p for p in ("spmv_pivot", "s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update", "true_res_p")
+            if p in phases]
+    dominant = max(body, key=lambda p: phases[p]["total_ms"])
+    dom_avg_s = prof[dominant][0] / prof[dominant][1] / 1e3
+    achieved = B[dominant] / dom_avg_s / 1e9
+    iter_s = sum(prof[p][0] for p in body) / max(prof["spmv_pivot"][1], 1) / 1e3
+    kernel_names = {"spmv_pivot": "k_spmv_pivot", "spmv_t": "k_spmv_t", "true_res_p": "k_true_res<1>",
+                    "s_update": "k_s_update", "xr_update": "k_xr_update"}
+
+    # ---- standalone kernels: zSpMV on C4, zdotc / zaxpy at 1e8 ------------------
+    rng = np.random.default_rng(42)
+    xs = Z.ZVector(rng.random(n) + 1j * rng.random(n))
+    y = Z.spmv(A, xs)
+    _lib.synchronize()
+    reps = 20
+    _lib.event_record(4)
+    for _ in range(reps):
+        Z.spmv(A, xs)
+    _lib.event_record(5)
+    spmv_ms = _lib.event_elapsed_ms(4, 5) / reps
+    nv = 100_000_000
+    v1 = Z.ZVector._device_new(nv)
+    v2 = Z.ZVector._device_new(nv)
+    _lib.check(_lib.lib().zk_memset(_lib.context(), v1._dptr_out(), 0, 16 * nv))
+    _lib.check(_lib.lib().zk_memset(_lib.context(), v2._dptr_out(), 0, 16 * nv))
+    Z.zdot(v1, v2)
+    _lib.event_record(6)
+    for _ in range(10):
+        Z.zdot(v1, v2)
+    _lib.event_record(7)
+    dot_ms = _lib.event_elapsed_ms(6, 7) / 10
+    _lib.event_record(8)
+    for _ in range(10):
+        Z.zaxpy(0.5 + 0.25j, v1, v2)
+    _lib.event_record(9)
+    axpy_ms = _lib.event_elapsed_ms(8, 9) / 10
+    del v1, v2, y
+
+    sub = {
+        "zspmv_gbs": round(B["spmv"] / (spmv_ms * 1e-3) / 1e9, 1),
+        "zspmv_frac": round(B["spmv"] / (spmv_ms * 1e-3) / 1e9 / peak, 3),
+        "zspmv_us": round(spmv_ms * 1e3, 1),
+        "zdotc_1e8_gbs": round(32 * nv / (dot_ms * 1e-3) / 1e9, 1),
+        "zdotc_1e8_frac": round(32 * nv / (dot_ms * 1e-3) / 1e9 / peak, 3),
+        "zaxpy_1e8_gbs": round(48 * nv / (axpy_ms * 1e-3) / 1e9, 1),
+        "zaxpy_1e8_frac": round(48 * nv / (axpy_ms * 1e-3) / 1e9 / peak, 3),
+        "bicgstab_iteration_gbs": round(B["iteration"] / iter_s / 1e9, 1),
+        "bicgstab_iteration_frac": round(B["iteration"] / iter_s / 1e9 / peak, 3),
+        "bicgstab_iteration_us": round(iter_s * 1e6, 1),
+        "phases": phases,
+    }
+
+    out = {
+        "metric": "bicgstab_solves_per_sec",
+        "value": round(value, 4),
+        "unit": "solves/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak" if dist.world > 1 else "strong",
+        "vs_baseline": None,
+        "dtype": "c128 (f64 re/im pairs)",
+        "data": "synthetic: generated 27-point Helmholtz stencil, unit interior source, zero Dirichlet",
+        "config": {
+            "workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8, x0=0",
+            "n": n, "nnz": nnz, "iterations": iters, "converged": bool(rep.converged),
+            "final_rel": rep.final_relative_residual,
+            "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (4.6 GB matrix, 126 MB L2): no flush",
+            "host_setup_s": round(setup_s, 1),
+        },
+        "e2e": {"value": round(dist.world / (e2e_step / 1e3), 4), "unit": "solves/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "ms_per_step": round(e2e_step, 3),
+                "path": "solve_bicgstab(CsrMatrix, ZVector, Preconditioner) from pinned host arrays, x.data read"},
+        "roofline": {"bound": "hbm", "kernel": kernel_names.get(dominant, dominant),
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 3), "peak_kind": peak_kind,
+                     "bytes_per_launch": int(B[dominant]), "avg_launch_us": round(dom_avg_s * 1e6, 1),
+                     "traffic": traffic_from_profiles(kernel_names.get(dominant, dominant))},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "sub_metrics": sub,
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(ia, ja, aa, b, M.data, iters)
+    if dist.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def cpu_sample(ia, ja, aa, b, minv, iters):
+    """One capped solve of the reference algorithm (oracle/port.py): setup +
+    one iteration; returns (solves/s extrapolated to `iters`, detail)."""
+    from oracle import port
+    t0 = time.perf_counter()
+    x, hist, conv, t_setup, it_times = port.bicgstab(ia, ja, aa, b, minv, TOL, 1)
+    wall = time.perf_counter() - t0
+    t_iter = it_times[0]
+    per_solve = t_setup + iters * t_iter
+    return 1.0 / per_solve, {"setup_s": t_setup, "iteration_s": t_iter, "wall_s": wall, "hist1": hist[-1]}
+
+
+def cpu_baseline(ia, ja, aa, b, minv, iters):
+    from oracle import fingerprint
+    v, d = cpu_sample(ia, ja, aa, b, minv, iters)
+    facts = fingerprint.host_facts()
+    return {"value": v, "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": (f"reference BiCGStab algorithm (oracle/port.py, numpy, single-threaded like zlinalg) on C4: "
+                       f"setup {d['setup_s']:.2f}s + 1 iteration {d['iteration_s']:.2f}s, extrapolated to "
+                       f"{iters} iterations"),
+            "host": facts}
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return
+    iters = args.iterations
+    if iters is None:
+        iters = C4_ITERATIONS_KNOWN
+    if iters is None:
+        print(json.dumps({"impl": "reference", "unavailable": "C4 iteration count unknown; pass --iterations"}))
+        return
+    n, ia, ja, aa, b = build_problem()
+    diag = np.zeros(n, dtype=np.complex128)
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ia))
+    hit = rows == ja
+    diag[rows[hit]] = aa[hit]
+    minv = np.divide(1.0, diag)  # build_jacobi (krylov.py:120)
+    from oracle import port
+    port.spmv(ia, ja, aa, b, n)  # warm-up (page-in)
+    vals, details = [], []
+    for _ in range(args.steps):
+        v, d = cpu_sample(ia, ja, aa, b, minv, iters)
+        vals.append(v)
+        details.append(d)
+    value = statistics.median(vals)
+    sample = (f"reference BiCGStab algorithm (oracle/port.py, numpy) on C4, per step: setup + 1 iteration "
+              f"(median iteration {statistics.median(d['iteration_s'] for d in details):.2f}s), extrapolated to "
+              f"{iters} iterations")
+    out = {"metric": "bicgstab_solves_per_sec", "value": value, "unit": "solves/s", "n_gpus": dist.world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": statistics.median(d["wall_s"] for d in details) * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64 re/im pairs)", "data": "synthetic",
+           "config": {"workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8",
+                      "iterations": iters},
+           "impl": "reference",
+           "cpu_baseline": {"value": value, "unit": "solves/s", "cores": 1, "kind": "port", "sample": sample},
+           "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["zk", "reference"], default="zk")
+    ap.add_argument("--iterations", type=int, default=None, help="reference arm: C4 iteration count")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    dist = Dist() if args.impl == "zk" else _NoDist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_zk(args, dist)
+    finally:
+        dist.close()
+
+
+class _NoDist(Dist):
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    def close(self):
+        pass
+
+
+if __name__ == "__main__":
+    main()

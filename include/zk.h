@@ -79,6 +79,23 @@ zk_status zk_launch_count(zk_context* ctx, int64_t* count);
 /* Launch stream as an opaque handle (cudaStream_t) for event timing. */
 zk_status zk_stream(zk_context* ctx, void** stream);
 
+/* Pin / unpin caller-owned host memory (cudaHostRegister) so uploads run at
+ * full PCIe rate. */
+zk_status zk_host_register(void* hptr, size_t bytes);
+zk_status zk_host_unregister(void* hptr);
+/* CUDA events on the context stream, slots 0..31 (device-side timing). */
+zk_status zk_event_record(zk_context* ctx, int slot);
+zk_status zk_event_elapsed(zk_context* ctx, int start_slot, int stop_slot, double* ms);
+
+/* Solver phase profiling.  While enabled, zk_bicgstab drives the loop from
+ * the host and brackets every phase kernel with CUDA events; zk_profile_read
+ * returns the accumulated device time and launch count per phase, in this
+ * order: setup, p_first, spmv_pivot, s_update, x_alpha, true_res_s, spmv_t,
+ * xr_update, true_res_p. */
+#define ZK_NPHASES 9
+zk_status zk_profile_enable(zk_context* ctx, int on);
+zk_status zk_profile_read(zk_context* ctx, double* total_ms, int64_t* launches);
+
 /* ---- level-1 kernels (vecops.py) ---------------------------------------- */
 /* zscal: x <- F1(x, alpha)                      replaces vecops.zscal  (vecops.py:124-127) */
 zk_status zk_zscal(zk_context* ctx, int64_t n, double alpha_re, double alpha_im, double* x);

@@ -76,6 +76,12 @@ SIGNATURES = {
     "zk_synchronize": [_vp],
     "zk_launch_count": [_vp, ctypes.POINTER(_i64)],
     "zk_stream": [_vp, ctypes.POINTER(_vp)],
+    "zk_host_register": [_vp, _sz],
+    "zk_host_unregister": [_vp],
+    "zk_event_record": [_vp, _i],
+    "zk_event_elapsed": [_vp, _i, _i, ctypes.POINTER(_d)],
+    "zk_profile_enable": [_vp, _i],
+    "zk_profile_read": [_vp, ctypes.POINTER(_d), ctypes.POINTER(_i64)],
     "zk_zscal": [_vp, _i64, _d, _d, _vp],
     "zk_zaxpy": [_vp, _i64, _d, _d, _vp, _vp],
     "zk_zaxmy": [_vp, _i64, _vp, _vp],
@@ -176,6 +182,39 @@ def launch_count() -> int:
     c = ctypes.c_int64()
     check(load_library().zk_launch_count(context(), ctypes.byref(c)))
     return c.value
+
+
+PHASES = ("setup", "p_first", "spmv_pivot", "s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update",
+          "true_res_p")
+
+
+def event_record(slot: int) -> None:
+    check(load_library().zk_event_record(context(), int(slot)))
+
+
+def event_elapsed_ms(start: int, stop: int) -> float:
+    ms = ctypes.c_double()
+    check(load_library().zk_event_elapsed(context(), int(start), int(stop), ctypes.byref(ms)))
+    return ms.value
+
+
+def profile_enable(on: bool) -> None:
+    check(load_library().zk_profile_enable(context(), int(bool(on))))
+
+
+def profile_read() -> dict:
+    ms = (ctypes.c_double * len(PHASES))()
+    cnt = (ctypes.c_int64 * len(PHASES))()
+    check(load_library().zk_profile_read(context(), ms, cnt))
+    return {name: (ms[i], cnt[i]) for i, name in enumerate(PHASES)}
+
+
+def host_register(arr) -> None:
+    check(load_library().zk_host_register(arr.ctypes.data, arr.nbytes))
+
+
+def host_unregister(arr) -> None:
+    check(load_library().zk_host_unregister(arr.ctypes.data))
 
 
 def synchronize() -> None:

@@ -99,6 +99,7 @@ void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y);
 int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
                     int64_t maxit, double2* x_out, double* history_host, zk_solve_report* rep);
 void destroy_solver_plan(zk_context* c, SolverPlan* P);
+void destroy_sell(zk_csr* A);
 
 }  // namespace zk
 
@@ -210,6 +211,8 @@ zk_status zk_context_destroy(zk_context* c) {
     return guarded([&] {
         if (!c) return;
         cudaStreamSynchronize(c->stream);
+        for (auto& e : c->events)
+            if (e) cudaEventDestroy(e);
         if (c->h_result) cudaFreeHost(c->h_result);
         cudaStreamDestroy(c->stream);
         delete c;
@@ -304,6 +307,62 @@ zk_status zk_stream(zk_context* c, void** stream) {
     });
 }
 
+zk_status zk_host_register(void* hptr, size_t bytes) {
+    return guarded([&] {
+        if (!hptr || !bytes) return;
+        ZK_CUDA(cudaHostRegister(hptr, bytes, cudaHostRegisterDefault));
+    });
+}
+
+zk_status zk_host_unregister(void* hptr) {
+    return guarded([&] {
+        if (!hptr) return;
+        ZK_CUDA(cudaHostUnregister(hptr));
+    });
+}
+
+zk_status zk_event_record(zk_context* c, int slot) {
+    return guarded([&] {
+        need_ctx(c);
+        need(slot >= 0 && slot < 32, ZK_ERR_PARAMETER, "event slot out of range");
+        if (!c->events[slot]) ZK_CUDA(cudaEventCreate(&c->events[slot]));
+        ZK_CUDA(cudaEventRecord(c->events[slot], c->stream));
+    });
+}
+
+zk_status zk_event_elapsed(zk_context* c, int a, int b, double* ms) {
+    return guarded([&] {
+        need_ctx(c);
+        need(a >= 0 && a < 32 && b >= 0 && b < 32 && c->events[a] && c->events[b], ZK_ERR_PARAMETER,
+             "event slot not recorded");
+        ZK_CUDA(cudaEventSynchronize(c->events[b]));
+        float f = 0.f;
+        ZK_CUDA(cudaEventElapsedTime(&f, c->events[a], c->events[b]));
+        *ms = f;
+    });
+}
+
+zk_status zk_profile_enable(zk_context* c, int on) {
+    return guarded([&] {
+        need_ctx(c);
+        c->profile = on != 0;
+        for (int i = 0; i < 16; ++i) {
+            c->prof_ms[i] = 0.0;
+            c->prof_n[i] = 0;
+        }
+    });
+}
+
+zk_status zk_profile_read(zk_context* c, double* total_ms, int64_t* launches) {
+    return guarded([&] {
+        need_ctx(c);
+        for (int i = 0; i < ZK_NPHASES; ++i) {
+            total_ms[i] = c->prof_ms[i];
+            launches[i] = c->prof_n[i];
+        }
+    });
+}
+
 zk_status zk_zscal(zk_context* c, int64_t n, double ar, double ai, double* x) {
     return guarded([&] {
         need_ctx(c);
@@ -393,7 +452,7 @@ zk_status zk_znorm2(zk_context* c, int64_t n, const double* x, int64_t block_siz
     });
 }
 
-static void validate_csr_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia, const int64_t* ja) {
+static void validate_csr_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia) {
     need(n_rows >= 0 && n_cols >= 0 && nnz >= 0, ZK_ERR_FORMAT, "negative dimensions");
     need(n_cols <= INT32_MAX, ZK_ERR_FORMAT, "n_cols exceeds the int32 column-index range of the device layout");
     if (n_rows == 0) {
@@ -403,8 +462,7 @@ static void validate_csr_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const
     need(ia != nullptr, ZK_ERR_FORMAT, "null row pointers");
     need(ia[0] == 0 && ia[n_rows] == nnz, ZK_ERR_FORMAT, "row pointers must span [0, nnz]");
     for (int64_t i = 0; i < n_rows; ++i) need(ia[i + 1] >= ia[i], ZK_ERR_FORMAT, "row pointers are not nondecreasing");
-    if (ja)
-        for (int64_t k = 0; k < nnz; ++k) need(ja[k] >= 0 && ja[k] < n_cols, ZK_ERR_FORMAT, "column index out of range");
+    // column indices are range-checked on the device while scattering (zk_spmv.cu)
 }
 
 zk_status zk_csr_create(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_host,
@@ -412,7 +470,7 @@ zk_status zk_csr_create(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t n
     return guarded([&] {
         need_ctx(c);
         need(out != nullptr, ZK_ERR_PARAMETER, "null output");
-        validate_csr_host(n_rows, n_cols, nnz, ia_host, ja_host);
+        validate_csr_host(n_rows, n_cols, nnz, ia_host);
         need(nnz == 0 || (ja_host && aa_host), ZK_ERR_FORMAT, "null column/value arrays");
         std::vector<int64_t> ia0;
         if (n_rows == 0) {
@@ -444,7 +502,7 @@ zk_status zk_csr_create_device(zk_context* c, int64_t n_rows, int64_t n_cols, in
         if (n_rows > 0)
             ZK_CUDA(cudaMemcpyAsync(ia_h.data(), ia, sizeof(int64_t) * (n_rows + 1), cudaMemcpyDeviceToHost, c->stream));
         ZK_CUDA(cudaStreamSynchronize(c->stream));
-        validate_csr_host(n_rows, n_cols, nnz, ia_h.data(), nullptr);
+        validate_csr_host(n_rows, n_cols, nnz, ia_h.data());
         *out = build_sell(c, n_rows, n_cols, nnz, ia_h.data(), ia, ja, D2(aa));
     });
 }
@@ -455,11 +513,7 @@ zk_status zk_csr_destroy(zk_csr* A) {
         zk_context* c = A->ctx;
         cudaStreamSynchronize(c->stream);
         for (int k = 0; k < 2; ++k) destroy_solver_plan(c, A->solver[k]);
-        void* ptrs[] = {A->aa, A->ja, A->slice_off, A->rowlen, A->long_row, A->long_blk_ptr,
-                        A->long_ia, A->long_ja, A->long_aa};
-        for (void* p : ptrs)
-            if (p) c->alloc.free(p);
-        delete A;
+        destroy_sell(A);
     });
 }
 

@@ -393,19 +393,51 @@ struct Launch {
     unsigned nb, ew;
 };
 
-void launch_prologue(const Launch& L, cudaStream_t s) {
+// Phase events for zk_profile_enable: ev[k] is recorded before phase k's
+// kernel and ev[k+1] after it (prologue phases 0-1, body phases 2-8).
+struct PhaseEvents {
+    cudaEvent_t ev[10] = {};
+    bool on = false;
+    void rec(int k, cudaStream_t s) {
+        if (on) ZK_CUDA(cudaEventRecord(ev[k], s));
+    }
+};
+
+void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
+    if (pe) pe->rec(0, s);
     k_setup<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc, L.pr);
+    if (pe) pe->rec(1, s);
     k_p_first<<<L.ew, kThreads, 0, s>>>(L.P->bufs);
+    if (pe) pe->rec(2, s);
 }
 
-void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond) {
+void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
+                 PhaseEvents* pe = nullptr) {
+    if (pe) pe->rec(2, s);
     k_spmv_pivot<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc);
+    if (pe) pe->rec(3, s);
     k_s_update<<<L.nb, kThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
+    if (pe) pe->rec(4, s);
     k_x_alpha<<<L.ew, kThreads, 0, s>>>(L.P->bufs);
+    if (pe) pe->rec(5, s);
     k_true_res<0><<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pr, cond, 0);
+    if (pe) pe->rec(6, s);
     k_spmv_t<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc);
+    if (pe) pe->rec(7, s);
     k_xr_update<<<L.nb, kThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
+    if (pe) pe->rec(8, s);
     k_true_res<1><<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pr, cond, use_cond);
+    if (pe) pe->rec(9, s);
+}
+
+void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
+    ZK_CUDA(cudaEventSynchronize(pe.ev[last + 1]));
+    for (int k = first; k <= last; ++k) {
+        float ms = 0.f;
+        ZK_CUDA(cudaEventElapsedTime(&ms, pe.ev[k], pe.ev[k + 1]));
+        c->prof_ms[k] += ms;
+        c->prof_n[k] += 1;
+    }
 }
 constexpr int kBodyKernels = 7;
 
@@ -541,21 +573,29 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     int64_t cap = (int64_t)num_sms() * 8;
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
     SolverState out;
-    if (use_graph()) {
+    if (use_graph() && !c->profile) {
         if (!P->graph_ok) build_graph(L);
         ZK_CUDA(cudaGraphLaunch(P->exec, s));
         ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
         ZK_CUDA(cudaStreamSynchronize(s));
-    } else {
-        launch_prologue(L, s);
+    } else {  // host-driven loop (ZK_SOLVER_LOOP=host, or phase profiling)
+        PhaseEvents pe;
+        pe.on = c->profile;
+        if (pe.on)
+            for (auto& e : pe.ev) ZK_CUDA(cudaEventCreate(&e));
+        launch_prologue(L, s, &pe);
         ZK_CUDA(cudaGetLastError());
+        if (pe.on) accumulate(c, pe, 0, 1);
         for (;;) {
-            launch_body(L, s, 0, 0);
+            launch_body(L, s, 0, 0, &pe);
             ZK_CUDA(cudaGetLastError());
             ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
             ZK_CUDA(cudaStreamSynchronize(s));
+            if (pe.on) accumulate(c, pe, 2, 8);
             if (out.done) break;
         }
+        if (pe.on)
+            for (auto& e : pe.ev) cudaEventDestroy(e);
     }
     c->launches += 2 + kBodyKernels * out.trips;
     const int64_t it = out.iterations;

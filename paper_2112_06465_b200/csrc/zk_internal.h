@@ -87,6 +87,10 @@ struct zk_context {
     double* d_result = nullptr;    // 4 doubles
     double* h_result = nullptr;    // pinned, 4 doubles
     int64_t launches = 0;          // kernels launched by this context
+    cudaEvent_t events[32] = {};   // zk_event_record slots
+    bool profile = false;          // zk_profile_enable
+    double prof_ms[16] = {};
+    int64_t prof_n[16] = {};
     std::mutex mu;
 
     char* plan(int32_t L, int32_t kind);

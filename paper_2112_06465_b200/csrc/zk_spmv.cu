@@ -32,33 +32,43 @@ namespace {
 
 // Scatter CSR rows into the SELL layout (thread per short row) and the side
 // CSR (thread per long row).  Setup only.
-__global__ void k_sell_scatter(int64_t n_rows, const int64_t* __restrict__ ia, const int64_t* __restrict__ ja,
-                               const double2* __restrict__ aa, const int64_t* __restrict__ slice_off,
-                               const uint8_t* __restrict__ rowlen, double2* __restrict__ saa,
-                               int32_t* __restrict__ sja) {
+// Column indices are range-checked here, on the device (the C ABI must not
+// trust them; a host loop over 200M+ entries would dominate an upload).
+__global__ void k_sell_scatter(int64_t n_rows, int64_t n_cols, const int64_t* __restrict__ ia,
+                               const int64_t* __restrict__ ja, const double2* __restrict__ aa,
+                               const int64_t* __restrict__ slice_off, const uint8_t* __restrict__ rowlen,
+                               double2* __restrict__ saa, int32_t* __restrict__ sja, unsigned int* bad) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n_rows) return;
     const int len = rowlen[row];
     if (len == 255) return;
     const int64_t base = slice_off[row / kSlice] + (row % kSlice);
     const int64_t lo = ia[row];
+    bool ok = true;
     for (int k = 0; k < len; ++k) {
+        const int64_t j = ja[lo + k];
+        ok &= (j >= 0) & (j < n_cols);
         saa[base + 32 * (int64_t)k] = aa[lo + k];
-        sja[base + 32 * (int64_t)k] = (int32_t)ja[lo + k];
+        sja[base + 32 * (int64_t)k] = ok ? (int32_t)j : 0;
     }
+    if (!ok) atomicOr(bad, 1u);
 }
 
-__global__ void k_long_scatter(int32_t n_long, const int32_t* __restrict__ long_row, const int64_t* __restrict__ ia,
-                               const int64_t* __restrict__ ja, const double2* __restrict__ aa,
-                               const int64_t* __restrict__ long_ia, int32_t* __restrict__ lja,
-                               double2* __restrict__ laa) {
+__global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __restrict__ long_row,
+                               const int64_t* __restrict__ ia, const int64_t* __restrict__ ja,
+                               const double2* __restrict__ aa, const int64_t* __restrict__ long_ia,
+                               int32_t* __restrict__ lja, double2* __restrict__ laa, unsigned int* bad) {
     const int li = blockIdx.x * blockDim.x + threadIdx.x;
     if (li >= n_long) return;
     const int64_t lo = ia[long_row[li]], len = long_ia[li + 1] - long_ia[li];
+    bool ok = true;
     for (int64_t k = 0; k < len; ++k) {
-        lja[long_ia[li] + k] = (int32_t)ja[lo + k];
+        const int64_t j = ja[lo + k];
+        ok &= (j >= 0) & (j < n_cols);
+        lja[long_ia[li] + k] = ok ? (int32_t)j : 0;
         laa[long_ia[li] + k] = aa[lo + k];
     }
+    if (!ok) atomicOr(bad, 1u);
 }
 
 __global__ void __launch_bounds__(kThreads) k_spmv(SellView A, const double2* __restrict__ x, double2* __restrict__ y) {
@@ -72,6 +82,15 @@ T* dalloc(zk_context* c, size_t count) {
 }
 
 }  // namespace
+
+void destroy_sell(zk_csr* A) {
+    zk_context* c = A->ctx;
+    void* ptrs[] = {A->aa, A->ja, A->slice_off, A->rowlen, A->long_row, A->long_blk_ptr,
+                    A->long_ia, A->long_ja, A->long_aa};
+    for (void* p : ptrs)
+        if (p) c->alloc.free(p);
+    delete A;
+}
 
 // Builds the SELL matrix from device CSR arrays and the host copy of ia.
 zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
@@ -122,8 +141,9 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
                             cudaMemcpyHostToDevice, st));
     ZK_CUDA(cudaMemcpyAsync(A->rowlen, rowlen.data(), nrp, cudaMemcpyHostToDevice, st));
     if (n_rows > 0) {
-        k_sell_scatter<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(n_rows, ia_d, ja_d, aa_d, A->slice_off,
-                                                                         A->rowlen, A->aa, A->ja);
+        k_sell_scatter<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(n_rows, n_cols, ia_d, ja_d, aa_d,
+                                                                         A->slice_off, A->rowlen, A->aa, A->ja,
+                                                                         c->counter + 1);
         ZK_CUDA(cudaGetLastError());
         c->launches++;
     }
@@ -138,17 +158,22 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
                                 cudaMemcpyHostToDevice, st));
         ZK_CUDA(cudaMemcpyAsync(A->long_ia, long_ia.data(), sizeof(int64_t) * long_ia.size(), cudaMemcpyHostToDevice,
                                 st));
-        k_long_scatter<<<(A->n_long + 255) / 256, 256, 0, st>>>(A->n_long, A->long_row, ia_d, ja_d, aa_d, A->long_ia,
-                                                               A->long_ja, A->long_aa);
+        k_long_scatter<<<(A->n_long + 255) / 256, 256, 0, st>>>(A->n_long, n_cols, A->long_row, ia_d, ja_d, aa_d,
+                                                               A->long_ia, A->long_ja, A->long_aa, c->counter + 1);
         ZK_CUDA(cudaGetLastError());
         c->launches++;
     }
     // host vectors are freed on return: wait for the async copies
+    unsigned int bad = 0;
+    ZK_CUDA(cudaMemcpyAsync(&bad, c->counter + 1, sizeof(bad), cudaMemcpyDeviceToHost, st));
     ZK_CUDA(cudaStreamSynchronize(st));
+    if (bad) {
+        ZK_CUDA(cudaMemsetAsync(c->counter + 1, 0, sizeof(unsigned int), st));
+        destroy_sell(A);
+        throw ZkError{ZK_ERR_FORMAT, "column index out of range"};
+    }
     return A;
 }
-
-void destroy_sell(zk_csr* A);
 
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
     if (A->n_rows == 0) return;
