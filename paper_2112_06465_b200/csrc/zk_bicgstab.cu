@@ -15,11 +15,14 @@
 //       fused with next iteration's p = ((p - omega v) * beta) + r, p^ = M p
 //                                                           -> fold: record, stop?
 //
-// Each phase is one kernel of one CTA per 4096-row block; the last CTA to
-// finish folds the block partials in order and runs the scalar recurrences
-// (Python Cplx arithmetic, zk_common.cuh) on a device SolverState.  The loop
-// is a CUDA-graph conditional WHILE node whose condition K61 sets, so a
-// whole solve is one graph launch and the host synchronises once.
+// SpMV phases are persistent TMA-pipelined kernels (zk_spmv.cuh); the
+// reduction of each 4096-row block runs on the consumer warps as soon as the
+// block's rows are done, while the producer warp keeps streaming the matrix.
+// The CTA that finishes the last block folds the block partials in order
+// and runs the scalar recurrences (Python Cplx arithmetic, zk_common.cuh) on
+// a device SolverState.  The loop is a CUDA-graph conditional WHILE node
+// whose condition K61 sets, so a solve is one graph launch and the host
+// synchronises once.
 #include <cstdlib>
 #include <cstring>
 
@@ -28,9 +31,9 @@
 
 namespace zk {
 
-SellView sell_view(const zk_csr* A, const zk_context* c);
-size_t reduce_smem_bytes(int nnodes, int nacc, size_t vbytes, int64_t fold_chunk);
-int plan_nnodes(zk_context* c, int32_t L, int32_t kind);
+SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra);
+size_t pipe_smem_bytes(const SellView& v, size_t extra);
+unsigned pipe_grid(const zk_csr* A);
 
 enum : int32_t { ST_RUNNING = 0, ST_CONVERGED = 1, ST_NOT_CONVERGED = 2, ST_BREAKDOWN = 3 };
 enum : int32_t { BD_NONE = 0, BD_RHO = 1, BD_OMEGA = 2, BD_PIVOT = 3, BD_TT = 4 };
@@ -53,10 +56,11 @@ struct SolverBufs {
     bool jacobi, fma;
 };
 
-constexpr int kStashBytes = kBlock * sizeof(double2);  // 64 KiB
-constexpr int kNodeBytes = 8 * 1024;                   // plan nodes (<= 129 nodes x 2 acc x 16 B)
-constexpr int kSpmvSmem = kStashBytes + kNodeBytes;
-constexpr int kEwSmem = 32 * 1024 + kNodeBytes;        // fold scratch (2048 x 16 B) + nodes
+constexpr int kStashC = kBlock * sizeof(double2);  // 64 KiB complex stash
+constexpr int kStashR = kBlock * sizeof(double);   // 32 KiB real stash
+constexpr int kNodeBytes = 8 * 1024;               // plan nodes (<= 129 nodes x 2 acc x 16 B)
+constexpr int kRedThreads = 288;                   // 65 complex leaves x 4 lanes fit one pass
+constexpr int kEwSmem = 32 * 1024 + kNodeBytes;    // fold scratch (2048 x 16 B) + nodes
 
 struct SolverPlan {
     int64_t n = 0;
@@ -70,6 +74,8 @@ struct SolverPlan {
 
 namespace {
 
+using Sync = GroupSync<kConsumers>;
+
 __device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
 
 __device__ __forceinline__ void stop(SolverState* st, int32_t status, int32_t what) {
@@ -78,8 +84,8 @@ __device__ __forceinline__ void stop(SolverState* st, int32_t status, int32_t wh
     st->done = 1;
 }
 
-// K1 body for one element: p = ((p + F1(-w, v)) * beta) + F1(1, r); p^ = F1(p, minv)
-// (krylov.py:263-266; zaxpy, zscal, zaxpy, M.apply -- three separate roundings).
+// p = ((p + F1(-w, v)) * beta) + F1(1, r); p^ = F1(p, minv)
+// (krylov.py:263-266: zaxpy, zscal, zaxpy, M.apply -- separate roundings).
 __device__ __forceinline__ void p_update(const SolverBufs& B, double2 mw, double2 beta, int64_t i) {
     const bool fma = B.fma;
     double2 p = B.p[i];
@@ -90,77 +96,148 @@ __device__ __forceinline__ void p_update(const SolverBufs& B, double2 mw, double
     if (B.jacobi) B.ph[i] = f1(p, __ldg(B.minv + i), fma);
 }
 
+// Reduction ops over the stash of the block just computed (smem reads only).
+struct StashNorm2 {  // |b|^2, |r0|^2 (setup)
+    const double2* b;
+    const double2* stash;
+    int64_t base;
+    struct Item { double2 b; };
+    static constexpr int U = 4;
+    __device__ Item load(int64_t e) const { return {b[e]}; }
+    __device__ void apply(int64_t e, const Item& it, double (&v)[2]) const {
+        v[0] = abs2_np(it.b);
+        v[1] = abs2_np(stash[e - base]);
+    }
+};
+
+struct StashSelfDot {  // <r0, r0> (setup)
+    const double2* stash;
+    int64_t base;
+    bool fma;
+    struct Item {};
+    static constexpr int U = 1;
+    __device__ Item load(int64_t) const { return {}; }
+    __device__ void apply(int64_t e, const Item&, double2 (&v)[1]) const {
+        double2 r0 = stash[e - base];
+        v[0] = f1(conjz(r0), r0, fma);
+    }
+};
+
+struct StashDot {  // <rs, stash> (pivot)
+    const double2* rs;
+    const double2* stash;
+    int64_t base;
+    bool fma;
+    struct Item { double2 r; };
+    static constexpr int U = 4;
+    __device__ Item load(int64_t e) const { return {__ldg(rs + e)}; }
+    __device__ void apply(int64_t e, const Item& it, double2 (&v)[1]) const {
+        v[0] = f1(conjz(it.r), stash[e - base], fma);
+    }
+};
+
+struct StashTT {  // <t, t>, <t, s>
+    const double2* s;
+    const double2* stash;
+    int64_t base;
+    bool fma;
+    struct Item { double2 s; };
+    static constexpr int U = 4;
+    __device__ Item load(int64_t e) const { return {s[e]}; }
+    __device__ void apply(int64_t e, const Item& it, double2 (&v)[2]) const {
+        double2 t = stash[e - base];
+        double2 ct = conjz(t);
+        v[0] = f1(ct, t, fma);
+        v[1] = f1(ct, it.s, fma);
+    }
+};
+
+struct StashReal {  // stashed |res|^2
+    const double* stash;
+    int64_t base;
+    struct Item {};
+    static constexpr int U = 1;
+    __device__ Item load(int64_t) const { return {}; }
+    __device__ void apply(int64_t e, const Item&, double (&v)[1]) const { v[0] = stash[e - base]; }
+};
+
 // ---- setup: r0 = b - A x0, ||b||, ||r0||, <r0, r0> (krylov.py:159-168, 255) ----
-__global__ void __launch_bounds__(kThreads) k_setup(SellView A, SolverBufs B, PlanPtrs pc, PlanPtrs pr) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double2* stash = reinterpret_cast<double2*>(smem);
-    SolverState* st = B.st;
-    if (st->done) return;
-    const int64_t blk = blockIdx.x, base = blk * kBlock;
-    const bool fma = B.fma;
-    auto epi = [&](int64_t row, double2 ax) {
-        double2 r0 = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, fma));
+struct SetupBody {
+    SolverBufs B;
+    PlanPtrs pc, pr;
+    double2* stash;
+    char* nodes;
+    unsigned int* flag;
+    double* res;
+    __device__ void row(int64_t row, double2 ax) {
+        const int64_t base = (row / kBlock) * kBlock;
+        double2 r0 = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, B.fma));
         B.r[row] = r0;
         B.rs[row] = r0;
         stash[row - base] = r0;
-    };
-    spmv_block(A, B.x, blk, epi);
-    __syncthreads();
-    double* nodes_r = reinterpret_cast<double*>(smem + kStashBytes);
-    auto fr = [&](int64_t e, double (&v)[2]) {
-        v[0] = abs2_np(B.b[e]);
-        v[1] = abs2_np(stash[e - base]);
-    };
-    double outr[2];
-    block_reduce<double, 2>(pr, B.n, kBlock, blk, fr, nodes_r, outr);
-    double2* nodes_c = reinterpret_cast<double2*>(smem + kStashBytes);
-    auto fc = [&](int64_t e, double2 (&v)[1]) {
-        double2 r0 = stash[e - base];
-        v[0] = f1(conjz(r0), r0, fma);
-    };
-    double2 outc[1];
-    block_reduce<double2, 1>(pc, B.n, kBlock, blk, fc, nodes_c, outc);
-    double* P = B.partials;
-    double2* PC = reinterpret_cast<double2*>(P + 2 * B.nblocks);
-    if (threadIdx.x == 0) {
-        P[2 * blk] = outr[0];
-        P[2 * blk + 1] = outr[1];
-        PC[blk] = outc[0];
     }
-    if (!arrive_last(&st->counter, gridDim.x)) return;
-    double tr[2];
-    ordered_fold<double>(P, 2, B.nblocks, reinterpret_cast<double*>(smem), 4096, tr);
-    double2 tc;
-    ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &tc);
-    if (threadIdx.x != 0) return;
-    st->counter = 0;
-    const double bn = __dsqrt_rn(tr[0]), rn = __dsqrt_rn(tr[1]);
-    st->b_norm = bn;
-    const double h0 = bn > 0.0 ? __ddiv_rn(rn, bn) : 0.0;
-    B.hist[0] = h0;
-    st->last_rel = h0;
-    if (bn == 0.0) {  // trivial_result: zero rhs -> x = 0, history [0.0]
-        B.hist[0] = 0.0;
-        st->last_rel = 0.0;
-        st->trivial_zero = 1;
-        stop(st, ST_CONVERGED, BD_NONE);
-        return;
+    __device__ void block_done(int64_t blk) {
+        const int64_t base = blk * kBlock;
+        double outr[2];
+        block_reduce<double, 2>(pr, B.n, kBlock, blk, StashNorm2{B.b, stash, base},
+                                reinterpret_cast<double*>(nodes), outr, Sync());
+        double2 outc[1];
+        block_reduce<double2, 1>(pc, B.n, kBlock, blk, StashSelfDot{stash, base, B.fma},
+                                 reinterpret_cast<double2*>(nodes), outc, Sync());
+        double* P = B.partials;
+        double2* PC = reinterpret_cast<double2*>(P + 2 * B.nblocks);
+        if (threadIdx.x == 0) {
+            P[2 * blk] = outr[0];
+            P[2 * blk + 1] = outr[1];
+            PC[blk] = outc[0];
+        }
+        SolverState* st = B.st;
+        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
+        double tr[2];
+        ordered_fold<double>(P, 2, B.nblocks, reinterpret_cast<double*>(stash), 4096, tr, res, Sync());
+        double2 tc;
+        ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &tc, res, Sync());
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        const double bn = __dsqrt_rn(tr[0]), rn = __dsqrt_rn(tr[1]);
+        st->b_norm = bn;
+        const double h0 = bn > 0.0 ? __ddiv_rn(rn, bn) : 0.0;
+        B.hist[0] = h0;
+        st->last_rel = h0;
+        if (bn == 0.0) {  // trivial_result: zero rhs -> x = 0, history [0.0]
+            B.hist[0] = 0.0;
+            st->last_rel = 0.0;
+            st->trivial_zero = 1;
+            stop(st, ST_CONVERGED, BD_NONE);
+            return;
+        }
+        if (h0 <= st->tol) {  // the initial guess already solves
+            stop(st, ST_CONVERGED, BD_NONE);
+            return;
+        }
+        // iteration 1: rho = alpha = omega = 1, no breakdown possible
+        const double2 one = make_double2(1.0, 0.0);
+        st->rho_old = one;
+        st->alpha = one;
+        st->omega = one;
+        st->beta = cmul_py(cdiv_py(tc, one), cdiv_py(one, one));
+        st->rho = tc;
     }
-    if (h0 <= st->tol) {  // initial guess already solves
-        stop(st, ST_CONVERGED, BD_NONE);
-        return;
-    }
-    // iteration 1: rho = alpha = omega = 1, no breakdown possible
-    const double2 one = make_double2(1.0, 0.0);
-    st->rho_old = one;
-    st->alpha = one;
-    st->omega = one;
-    st->beta = cmul_py(cdiv_py(tc, one), cdiv_py(one, one));
-    st->rho = tc;
+};
+
+__global__ void __launch_bounds__(kPipeThreads, 1) k_setup(SellView A, SolverBufs B, PlanPtrs pc, PlanPtrs pr) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
+    if (B.st->done) return;
+    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
+    SetupBody body{B, pc, pr, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag,
+                   s_res};
+    sell_pipeline(A, B.x, body, smem);
 }
 
 // ---- K1: p update for the first iteration (p = v = 0) ----
-__global__ void __launch_bounds__(kThreads) k_p_first(SolverBufs B) {
+__global__ void __launch_bounds__(256) k_p_first(SolverBufs B) {
     const SolverState* st = B.st;
     if (st->done) return;
     const double2 mw = neg(st->omega), beta = st->beta;
@@ -169,66 +246,98 @@ __global__ void __launch_bounds__(kThreads) k_p_first(SolverBufs B) {
 }
 
 // ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
-__global__ void __launch_bounds__(kThreads) k_spmv_pivot(SellView A, SolverBufs B, PlanPtrs pc) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double2* stash = reinterpret_cast<double2*>(smem);
+struct PivotBody {
+    SolverBufs B;
+    PlanPtrs pc;
+    double2* stash;
+    char* nodes;
+    unsigned int* flag;
+    double* res;
+    __device__ void row(int64_t row, double2 av) {
+        B.v[row] = av;
+        stash[row - (row / kBlock) * kBlock] = av;
+    }
+    __device__ void block_done(int64_t blk) {
+        const int64_t base = blk * kBlock;
+        double2 out[1];
+        block_reduce<double2, 1>(pc, B.n, kBlock, blk, StashDot{B.rs, stash, base, B.fma},
+                                 reinterpret_cast<double2*>(nodes), out, Sync());
+        double2* PC = reinterpret_cast<double2*>(B.partials);
+        if (threadIdx.x == 0) PC[blk] = out[0];
+        SolverState* st = B.st;
+        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
+        double2 pivot;
+        ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &pivot, res, Sync());
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        if (small_py(pivot)) {
+            stop(st, ST_BREAKDOWN, BD_PIVOT);
+            return;
+        }
+        st->alpha = cdiv_py(st->rho, pivot);
+    }
+};
+
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_pivot(SellView A, SolverBufs B, PlanPtrs pc) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;
     if (st->done) return;
-    const int64_t blk = blockIdx.x, base = blk * kBlock;
-    const bool fma = B.fma;
-    auto epi = [&](int64_t row, double2 av) {
-        B.v[row] = av;
-        stash[row - base] = av;
-    };
-    spmv_block(A, B.ph, blk, epi);
-    __syncthreads();
-    double2* nodes = reinterpret_cast<double2*>(smem + kStashBytes);
-    auto f = [&](int64_t e, double2 (&v)[1]) { v[0] = f1(conjz(__ldg(B.rs + e)), stash[e - base], fma); };
-    double2 out[1];
-    block_reduce<double2, 1>(pc, B.n, kBlock, blk, f, nodes, out);
-    double2* PC = reinterpret_cast<double2*>(B.partials);
-    if (threadIdx.x == 0) PC[blk] = out[0];
-    if (!arrive_last(&st->counter, gridDim.x)) return;
-    double2 pivot;
-    ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &pivot);
-    if (threadIdx.x != 0) return;
-    st->counter = 0;
-    if (small_py(pivot)) {
-        stop(st, ST_BREAKDOWN, BD_PIVOT);
-        return;
-    }
-    st->alpha = cdiv_py(st->rho, pivot);
+    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
+    PivotBody body{B, pc, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag,
+                   s_res};
+    sell_pipeline(A, B.ph, body, smem);
 }
 
 // ---- K3: s = r + F1(-alpha, v); s^ = M s; ||s|| -> s-check (krylov.py:272-275) ----
-__global__ void __launch_bounds__(kThreads) k_s_update(SolverBufs B, PlanPtrs pr) {
-    extern __shared__ __align__(16) unsigned char smem[];
+struct SUpdateOp {
+    const double2* r;
+    const double2* v;
+    const double2* minv;
+    double2* s;
+    double2* sh;
+    double2 ma;
+    bool jacobi, fma;
+    struct Item { double2 r, v, m; };
+    static constexpr int U = 4;
+    __device__ Item load(int64_t e) const {
+        Item it;
+        it.r = r[e];
+        it.v = v[e];
+        if (jacobi) it.m = __ldg(minv + e);
+        return it;
+    }
+    __device__ void apply(int64_t e, const Item& it, double (&out)[1]) const {
+        double2 sv = cadd(it.r, f1(ma, it.v, fma));
+        s[e] = sv;
+        if (jacobi) sh[e] = f1(sv, it.m, fma);
+        out[0] = abs2_np(sv);
+    }
+};
+
+__global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (st->done) return;
     const int64_t blk = blockIdx.x;
-    const bool fma = B.fma;
-    const double2 ma = neg(st->alpha);
-    auto f = [&](int64_t e, double (&v)[1]) {
-        double2 s = cadd(B.r[e], f1(ma, B.v[e], fma));
-        B.s[e] = s;
-        if (B.jacobi) B.sh[e] = f1(s, __ldg(B.minv + e), fma);
-        v[0] = abs2_np(s);
-    };
-    double* nodes = reinterpret_cast<double*>(smem + 32 * 1024);
+    SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
     double out[1];
-    block_reduce<double, 1>(pr, B.n, kBlock, blk, f, nodes, out);
+    block_reduce<double, 1>(pr, B.n, kBlock, blk, op, reinterpret_cast<double*>(smem + 32 * 1024), out);
     if (threadIdx.x == 0) B.partials[blk] = out[0];
-    if (!arrive_last(&st->counter, gridDim.x)) return;
+    if (!arrive_last(&st->counter, gridDim.x, &s_flag)) return;
     double ss;
-    ordered_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), 4096, &ss);
+    ordered_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), 4096, &ss, s_res);
     if (threadIdx.x != 0) return;
     st->counter = 0;
     st->scheck = (__ddiv_rn(__dsqrt_rn(ss), st->b_norm) <= st->tol) ? 1 : 0;
 }
 
 // ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
-__global__ void __launch_bounds__(kThreads) k_x_alpha(SolverBufs B) {
+__global__ void __launch_bounds__(256) k_x_alpha(SolverBufs B) {
     SolverState* st = B.st;
     if (st->done || !st->scheck) return;
     const double2 a = st->alpha;
@@ -239,133 +348,179 @@ __global__ void __launch_bounds__(kThreads) k_x_alpha(SolverBufs B) {
 }
 
 // ---- true residual ||b + F1(-1, A x)|| / ||b|| (krylov.py:183-186) ----
-// mode 0: on the s-check path (K6x);  mode 1: end of iteration (K61), fused
+// MODE 0: on the s-check path (K6x);  MODE 1: end of iteration (K61), fused
 // with the next iteration's p update.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_true_res(SellView A, SolverBufs B, PlanPtrs pr,
-                                                       cudaGraphConditionalHandle cond, int use_cond) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double* stash = reinterpret_cast<double*>(smem);
+struct ResBody {
+    SolverBufs B;
+    PlanPtrs pr;
+    double* stash;
+    char* nodes;
+    unsigned int* flag;
+    double* res;
+    double2 mw, beta;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+    __device__ void row(int64_t row, double2 ax) {
+        double2 rv = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, B.fma));
+        stash[row - (row / kBlock) * kBlock] = abs2_np(rv);
+        if (MODE == 1) p_update(B, mw, beta, row);
+    }
+    __device__ void block_done(int64_t blk) {
+        const int64_t base = blk * kBlock;
+        double out[1];
+        block_reduce<double, 1>(pr, B.n, kBlock, blk, StashReal{stash, base}, reinterpret_cast<double*>(nodes), out,
+                                Sync());
+        if (threadIdx.x == 0) B.partials[blk] = out[0];
+        SolverState* st = B.st;
+        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
+        double rr;
+        ordered_fold<double>(B.partials, 1, B.nblocks, stash, 4096, &rr, res, Sync());
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        const double rel = __ddiv_rn(__dsqrt_rn(rr), st->b_norm);
+        if (MODE == 0) {
+            if (rel <= st->tol) {
+                st->iterations++;
+                B.hist[st->iterations] = rel;
+                st->last_rel = rel;
+                stop(st, ST_CONVERGED, BD_NONE);
+            }
+            return;
+        }
+        st->iterations++;
+        B.hist[st->iterations] = rel;
+        st->last_rel = rel;
+        st->scheck = 0;
+        st->alpha_applied = 0;
+        if (rel <= st->tol) {
+            stop(st, ST_CONVERGED, BD_NONE);
+        } else if (st->iterations >= st->maxit) {
+            stop(st, ST_NOT_CONVERGED, BD_NONE);
+        } else if (small_py(st->rho_old)) {  // next iteration's checks (krylov.py:256-259)
+            stop(st, ST_BREAKDOWN, BD_RHO);
+        } else if (small_py(st->omega)) {
+            stop(st, ST_BREAKDOWN, BD_OMEGA);
+        }
+        if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+    }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kPipeThreads, 1) k_true_res(SellView A, SolverBufs B, PlanPtrs pr,
+                                                              cudaGraphConditionalHandle cond, int use_cond) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (st->done || (MODE == 0 && !st->scheck)) {
         if (MODE == 1 && use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
         return;
     }
-    const int64_t blk = blockIdx.x, base = blk * kBlock;
-    const bool fma = B.fma;
-    const double2 mw = neg(st->omega), beta = st->beta;
-    auto epi = [&](int64_t row, double2 ax) {
-        double2 res = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, fma));
-        stash[row - base] = abs2_np(res);
-        if (MODE == 1) p_update(B, mw, beta, row);
-    };
-    spmv_block(A, B.x, blk, epi);
-    __syncthreads();
-    double* nodes = reinterpret_cast<double*>(smem + kStashBytes);
-    auto f = [&](int64_t e, double (&v)[1]) { v[0] = stash[e - base]; };
-    double out[1];
-    block_reduce<double, 1>(pr, B.n, kBlock, blk, f, nodes, out);
-    if (threadIdx.x == 0) B.partials[blk] = out[0];
-    if (!arrive_last(&st->counter, gridDim.x)) return;
-    double rr;
-    ordered_fold<double>(B.partials, 1, B.nblocks, stash, 4096, &rr);
-    if (threadIdx.x != 0) return;
-    st->counter = 0;
-    const double rel = __ddiv_rn(__dsqrt_rn(rr), st->b_norm);
-    if (MODE == 0) {
-        if (rel <= st->tol) {
-            st->iterations++;
-            B.hist[st->iterations] = rel;
-            st->last_rel = rel;
-            stop(st, ST_CONVERGED, BD_NONE);
-        }
-        return;
-    }
-    st->iterations++;
-    B.hist[st->iterations] = rel;
-    st->last_rel = rel;
-    st->scheck = 0;
-    st->alpha_applied = 0;
-    if (rel <= st->tol) {
-        stop(st, ST_CONVERGED, BD_NONE);
-    } else if (st->iterations >= st->maxit) {
-        stop(st, ST_NOT_CONVERGED, BD_NONE);
-    } else if (small_py(st->rho_old)) {  // next iteration's checks (krylov.py:256-259)
-        stop(st, ST_BREAKDOWN, BD_RHO);
-    } else if (small_py(st->omega)) {
-        stop(st, ST_BREAKDOWN, BD_OMEGA);
-    }
-    if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
+    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
+    ResBody<MODE> body{B, pr, reinterpret_cast<double*>(extra), reinterpret_cast<char*>(extra + kStashR), &s_flag,
+                       s_res, neg(st->omega), st->beta, cond, use_cond};
+    sell_pipeline(A, B.x, body, smem);
 }
 
 // ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
-__global__ void __launch_bounds__(kThreads) k_spmv_t(SellView A, SolverBufs B, PlanPtrs pc) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    double2* stash = reinterpret_cast<double2*>(smem);
-    SolverState* st = B.st;
-    if (st->done) return;
-    const int64_t blk = blockIdx.x, base = blk * kBlock;
-    const bool fma = B.fma;
-    auto epi = [&](int64_t row, double2 at) {
+struct TBody {
+    SolverBufs B;
+    PlanPtrs pc;
+    double2* stash;
+    char* nodes;
+    unsigned int* flag;
+    double* res;
+    __device__ void row(int64_t row, double2 at) {
         B.t[row] = at;
-        stash[row - base] = at;
-    };
-    spmv_block(A, B.sh, blk, epi);
-    __syncthreads();
-    double2* nodes = reinterpret_cast<double2*>(smem + kStashBytes);
-    auto f = [&](int64_t e, double2 (&v)[2]) {
-        double2 t = stash[e - base];
-        double2 ct = conjz(t);
-        v[0] = f1(ct, t, fma);
-        v[1] = f1(ct, B.s[e], fma);
-    };
-    double2 out[2];
-    block_reduce<double2, 2>(pc, B.n, kBlock, blk, f, nodes, out);
-    double2* PC = reinterpret_cast<double2*>(B.partials);
-    if (threadIdx.x == 0) {
-        PC[2 * blk] = out[0];
-        PC[2 * blk + 1] = out[1];
+        stash[row - (row / kBlock) * kBlock] = at;
     }
-    if (!arrive_last(&st->counter, gridDim.x)) return;
-    double2 tot[2];
-    ordered_fold<double2>(PC, 2, B.nblocks, stash, 2048, tot);
-    if (threadIdx.x != 0) return;
-    st->counter = 0;
-    if (small_py(tot[0])) {
-        stop(st, ST_BREAKDOWN, BD_TT);
-        return;
+    __device__ void block_done(int64_t blk) {
+        const int64_t base = blk * kBlock;
+        double2 out[2];
+        block_reduce<double2, 2>(pc, B.n, kBlock, blk, StashTT{B.s, stash, base, B.fma},
+                                 reinterpret_cast<double2*>(nodes), out, Sync());
+        double2* PC = reinterpret_cast<double2*>(B.partials);
+        if (threadIdx.x == 0) {
+            PC[2 * blk] = out[0];
+            PC[2 * blk + 1] = out[1];
+        }
+        SolverState* st = B.st;
+        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
+        double2 tot[2];
+        ordered_fold<double2>(PC, 2, B.nblocks, stash, 2048, tot, res, Sync());
+        if (threadIdx.x != 0) return;
+        st->counter = 0;
+        if (small_py(tot[0])) {
+            stop(st, ST_BREAKDOWN, BD_TT);
+            return;
+        }
+        const double2 w = cdiv_py(tot[1], tot[0]);
+        st->omega = w;
+        if (small_py(w)) stop(st, ST_BREAKDOWN, BD_OMEGA);
     }
-    const double2 w = cdiv_py(tot[1], tot[0]);
-    st->omega = w;
-    if (small_py(w)) stop(st, ST_BREAKDOWN, BD_OMEGA);
+};
+
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_t(SellView A, SolverBufs B, PlanPtrs pc) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
+    if (B.st->done) return;
+    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
+    TBody body{B, pc, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag, s_res};
+    sell_pipeline(A, B.sh, body, smem);
 }
 
 // ---- K5: x, r updates and <r~, r> -> rho', beta (krylov.py:288-290, 255-261) ----
-__global__ void __launch_bounds__(kThreads) k_xr_update(SolverBufs B, PlanPtrs pc) {
-    extern __shared__ __align__(16) unsigned char smem[];
+struct XrOp {
+    double2* x;
+    double2* r;
+    const double2* ph;
+    const double2* sh;
+    const double2* s;
+    const double2* t;
+    const double2* rs;
+    double2 a, w, mw;
+    bool applied, fma;
+    struct Item { double2 x, ph, sh, s, t, rs; };
+    static constexpr int U = 2;
+    __device__ Item load(int64_t e) const {
+        Item it;
+        it.x = x[e];
+        if (!applied) it.ph = ph[e];
+        it.sh = sh[e];
+        it.s = s[e];
+        it.t = t[e];
+        it.rs = __ldg(rs + e);
+        return it;
+    }
+    __device__ void apply(int64_t e, const Item& it, double2 (&v)[1]) const {
+        double2 xv = it.x;
+        if (!applied) xv = cadd(xv, f1(a, it.ph, fma));
+        xv = cadd(xv, f1(w, it.sh, fma));
+        x[e] = xv;
+        double2 rv = cadd(it.s, f1(mw, it.t, fma));
+        r[e] = rv;
+        v[0] = f1(conjz(it.rs), rv, fma);
+    }
+};
+
+__global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, PlanPtrs pc) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (st->done) return;
     const int64_t blk = blockIdx.x;
-    const bool fma = B.fma;
-    const double2 a = st->alpha, w = st->omega, mw = neg(w);
-    const bool applied = st->alpha_applied != 0;
-    auto f = [&](int64_t e, double2 (&v)[1]) {
-        double2 xv = B.x[e];
-        if (!applied) xv = cadd(xv, f1(a, B.ph[e], fma));
-        xv = cadd(xv, f1(w, B.sh[e], fma));
-        B.x[e] = xv;
-        double2 rv = cadd(B.s[e], f1(mw, B.t[e], fma));
-        B.r[e] = rv;
-        v[0] = f1(conjz(__ldg(B.rs + e)), rv, fma);
-    };
-    double2* nodes = reinterpret_cast<double2*>(smem + 32 * 1024);
+    const double2 a = st->alpha, w = st->omega;
+    XrOp op{B.x, B.r, B.ph, B.sh, B.s, B.t, B.rs, a, w, neg(w), st->alpha_applied != 0, B.fma};
     double2 out[1];
-    block_reduce<double2, 1>(pc, B.n, kBlock, blk, f, nodes, out);
+    block_reduce<double2, 1>(pc, B.n, kBlock, blk, op, reinterpret_cast<double2*>(smem + 32 * 1024), out);
     double2* PC = reinterpret_cast<double2*>(B.partials);
     if (threadIdx.x == 0) PC[blk] = out[0];
-    if (!arrive_last(&st->counter, gridDim.x)) return;
+    if (!arrive_last(&st->counter, gridDim.x, &s_flag)) return;
     double2 rho_next;
-    ordered_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), 2048, &rho_next);
+    ordered_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), 2048, &rho_next, s_res);
     if (threadIdx.x != 0) return;
     st->counter = 0;
     const double2 rho = st->rho;
@@ -381,16 +536,17 @@ __global__ void __launch_bounds__(kThreads) k_xr_update(SolverBufs B, PlanPtrs p
 namespace {
 
 template <class K>
-void smem_attr(K kernel, int bytes) {
-    ZK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+void smem_attr(K kernel, size_t bytes) {
+    ZK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 struct Launch {
     zk_context* c;
     SolverPlan* P;
-    SellView A;
+    SellView Ac, Ar;        // ring geometry with a complex / real stash
+    size_t smem_c, smem_r;  // dynamic smem of the SpMV-phase kernels
     PlanPtrs pc, pr;
-    unsigned nb, ew;
+    unsigned nb, ew, pg;
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
@@ -405,30 +561,31 @@ struct PhaseEvents {
 
 void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(0, s);
-    k_setup<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc, L.pr);
+    k_setup<<<L.pg, kPipeThreads, L.smem_c, s>>>(L.Ac, L.P->bufs, L.pc, L.pr);
     if (pe) pe->rec(1, s);
-    k_p_first<<<L.ew, kThreads, 0, s>>>(L.P->bufs);
+    k_p_first<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(2, s);
 }
 
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(2, s);
-    k_spmv_pivot<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc);
+    k_spmv_pivot<<<L.pg, kPipeThreads, L.smem_c, s>>>(L.Ac, L.P->bufs, L.pc);
     if (pe) pe->rec(3, s);
-    k_s_update<<<L.nb, kThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
+    k_s_update<<<L.nb, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
     if (pe) pe->rec(4, s);
-    k_x_alpha<<<L.ew, kThreads, 0, s>>>(L.P->bufs);
+    k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(5, s);
-    k_true_res<0><<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pr, cond, 0);
+    k_true_res<0><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, 0);
     if (pe) pe->rec(6, s);
-    k_spmv_t<<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pc);
+    k_spmv_t<<<L.pg, kPipeThreads, L.smem_c, s>>>(L.Ac, L.P->bufs, L.pc);
     if (pe) pe->rec(7, s);
-    k_xr_update<<<L.nb, kThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
+    k_xr_update<<<L.nb, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
     if (pe) pe->rec(8, s);
-    k_true_res<1><<<L.nb, kThreads, kSpmvSmem, s>>>(L.A, L.P->bufs, L.pr, cond, use_cond);
+    k_true_res<1><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, use_cond);
     if (pe) pe->rec(9, s);
 }
+constexpr int kBodyKernels = 7;
 
 void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
     ZK_CUDA(cudaEventSynchronize(pe.ev[last + 1]));
@@ -439,19 +596,15 @@ void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
         c->prof_n[k] += 1;
     }
 }
-constexpr int kBodyKernels = 7;
 
-bool g_attrs_done = false;
-void set_attrs() {
-    if (g_attrs_done) return;
-    smem_attr(k_setup, kSpmvSmem);
-    smem_attr(k_spmv_pivot, kSpmvSmem);
-    smem_attr(k_true_res<0>, kSpmvSmem);
-    smem_attr(k_true_res<1>, kSpmvSmem);
-    smem_attr(k_spmv_t, kSpmvSmem);
+void set_attrs(const Launch& L) {
+    smem_attr(k_setup, L.smem_c);
+    smem_attr(k_spmv_pivot, L.smem_c);
+    smem_attr(k_spmv_t, L.smem_c);
+    smem_attr(k_true_res<0>, L.smem_r);
+    smem_attr(k_true_res<1>, L.smem_r);
     smem_attr(k_s_update, kEwSmem);
     smem_attr(k_xr_update, kEwSmem);
-    g_attrs_done = true;
 }
 
 bool use_graph() {
@@ -542,7 +695,6 @@ static SolverPlan* get_plan(zk_context* c, zk_csr* A, bool jacobi, int64_t maxit
 int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
                     int64_t maxit, double2* x_out, double* history_host, zk_solve_report* rep) {
     const int64_t n = A->n_rows;
-    set_attrs();
     SolverPlan* P = get_plan(c, A, minv != nullptr, maxit);
     SolverBufs& B = P->bufs;
     if (B.fma != (c->fma != 0)) {  // fingerprint changed since the graph was built
@@ -567,11 +719,21 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     h.maxit = maxit;
     ZK_CUDA(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
 
-    Launch L{c, P, sell_view(A, c), c->plans_for(n, kBlock, kComplex), c->plans_for(n, kBlock, kReal),
-             (unsigned)B.nblocks, 0};
-    int64_t ewg = (n + kThreads - 1) / kThreads;
+    Launch L;
+    L.c = c;
+    L.P = P;
+    L.Ac = sell_view(A, c, kStashC + kNodeBytes);
+    L.Ar = sell_view(A, c, kStashR + kNodeBytes);
+    L.smem_c = pipe_smem_bytes(L.Ac, kStashC + kNodeBytes);
+    L.smem_r = pipe_smem_bytes(L.Ar, kStashR + kNodeBytes);
+    L.pc = c->plans_for(n, kBlock, kComplex);
+    L.pr = c->plans_for(n, kBlock, kReal);
+    L.nb = (unsigned)B.nblocks;
+    L.pg = pipe_grid(A);
+    int64_t ewg = (n + 255) / 256;
     int64_t cap = (int64_t)num_sms() * 8;
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
+    set_attrs(L);
     SolverState out;
     if (use_graph() && !c->profile) {
         if (!P->graph_ok) build_graph(L);

@@ -50,23 +50,44 @@ __global__ void k_jacobi(int64_t n, const double2* __restrict__ v, const double2
     ew_loop(n, [&](int64_t i) { out[i] = f1(ldg2(v + i), ldg2(m + i), fma); });
 }
 
-// Blocked zdot: one CTA per block; last CTA folds the partials.
-__global__ void __launch_bounds__(kThreads) k_zdot_blocked(int64_t n, const double2* __restrict__ x,
-                                                           const double2* __restrict__ y, bool conj,
-                                                           int64_t block, PlanPtrs plans, double2* partials,
-                                                           unsigned int* counter, double2* result, bool fma) {
+constexpr int kRedThreads = 288;  // 65 complex / 33 real leaves x lanes fit one pass
+
+struct DotOp {
+    const double2* __restrict__ x;
+    const double2* __restrict__ y;
+    bool conj, fma;
+    struct Item { double2 x, y; };
+    static constexpr int U = 8;
+    __device__ Item load(int64_t e) const { return {__ldg(x + e), __ldg(y + e)}; }
+    __device__ void apply(int64_t, const Item& it, double2 (&v)[1]) const {
+        double2 a = it.x;
+        if (conj) a.y = -a.y;  // np.conj
+        v[0] = f1(a, it.y, fma);
+    }
+};
+
+struct Norm2Op {
+    const double2* __restrict__ x;
+    struct Item { double2 x; };
+    static constexpr int U = 8;
+    __device__ Item load(int64_t e) const { return {__ldg(x + e)}; }
+    __device__ void apply(int64_t, const Item& it, double (&v)[1]) const { v[0] = abs2_np(it.x); }
+};
+
+// Blocked zdot: one CTA per reduction block; the last CTA folds the partials.
+__global__ void __launch_bounds__(kRedThreads, 2) k_zdot_blocked(int64_t n, const double2* __restrict__ x,
+                                                              const double2* __restrict__ y, bool conj,
+                                                              int64_t block, PlanPtrs plans, double2* partials,
+                                                              unsigned int* counter, double2* result, bool fma) {
     extern __shared__ double2 smem_c[];
-    auto f = [&](int64_t e, double2 (&v)[1]) {
-        double2 a = ldg2(x + e);
-        if (conj) a.y = -a.y;
-        v[0] = f1(a, ldg2(y + e), fma);
-    };
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
     double2 out[1];
-    block_reduce<double2, 1>(plans, n, block, blockIdx.x, f, smem_c, out);
+    block_reduce<double2, 1>(plans, n, block, blockIdx.x, DotOp{x, y, conj, fma}, smem_c, out);
     if (threadIdx.x == 0) partials[blockIdx.x] = out[0];
-    if (arrive_last(counter, gridDim.x)) {
+    if (arrive_last(counter, gridDim.x, &s_flag)) {
         double2 tot;
-        ordered_fold<double2>(partials, 1, gridDim.x, smem_c, 2048, &tot);
+        ordered_fold<double2>(partials, 1, gridDim.x, smem_c, 2048, &tot, s_res);
         if (threadIdx.x == 0) {
             *result = tot;
             *counter = 0;
@@ -74,17 +95,18 @@ __global__ void __launch_bounds__(kThreads) k_zdot_blocked(int64_t n, const doub
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_znorm2_blocked(int64_t n, const double2* __restrict__ x,
-                                                             int64_t block, PlanPtrs plans, double* partials,
-                                                             unsigned int* counter, double* result) {
+__global__ void __launch_bounds__(kRedThreads, 3) k_znorm2_blocked(int64_t n, const double2* __restrict__ x,
+                                                                int64_t block, PlanPtrs plans, double* partials,
+                                                                unsigned int* counter, double* result) {
     extern __shared__ double smem_r[];
-    auto f = [&](int64_t e, double (&v)[1]) { v[0] = abs2_np(ldg2(x + e)); };
+    __shared__ unsigned int s_flag;
+    __shared__ double s_res[16];
     double out[1];
-    block_reduce<double, 1>(plans, n, block, blockIdx.x, f, smem_r, out);
+    block_reduce<double, 1>(plans, n, block, blockIdx.x, Norm2Op{x}, smem_r, out);
     if (threadIdx.x == 0) partials[blockIdx.x] = out[0];
-    if (arrive_last(counter, gridDim.x)) {
+    if (arrive_last(counter, gridDim.x, &s_flag)) {
         double tot;
-        ordered_fold<double>(partials, 1, gridDim.x, smem_r, 4096, &tot);
+        ordered_fold<double>(partials, 1, gridDim.x, smem_r, 4096, &tot, s_res);
         if (threadIdx.x == 0) {
             *result = __dsqrt_rn(tot);
             *counter = 0;
@@ -169,7 +191,7 @@ void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, b
     double2* partials = static_cast<double2*>(c->scratch_partials(sizeof(double2) * nb));
     if (smem > 48 * 1024)
         ZK_CUDA(cudaFuncSetAttribute(k_zdot_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_zdot_blocked<<<(unsigned)nb, kThreads, smem, c->stream>>>(n, x, y, conj, block, p, partials, c->counter,
+    k_zdot_blocked<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, x, y, conj, block, p, partials, c->counter,
                                                                  result, c->fma);
     ZK_CUDA(cudaGetLastError());
     c->launches++;
@@ -192,7 +214,7 @@ void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, in
     double* partials = static_cast<double*>(c->scratch_partials(sizeof(double) * nb));
     if (smem > 48 * 1024)
         ZK_CUDA(cudaFuncSetAttribute(k_znorm2_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_znorm2_blocked<<<(unsigned)nb, kThreads, smem, c->stream>>>(n, x, block, p, partials, c->counter, result);
+    k_znorm2_blocked<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, x, block, p, partials, c->counter, result);
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }

@@ -60,6 +60,7 @@ struct zk_csr {
     int64_t n_rows, n_cols, nnz;
     int64_t nslices, nblocks;       // 32-row slices, 4096-row blocks
     int64_t sell_elems;             // padded element count
+    int32_t wmax;                   // widest slice (entries per row)
     double2* aa;                    // [sell_elems]
     int32_t* ja;                    // [sell_elems]
     int64_t* slice_off;             // [nslices + 1]

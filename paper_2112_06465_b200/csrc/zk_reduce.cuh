@@ -1,21 +1,27 @@
 // zk_reduce.cuh -- per-block numpy-order reductions and the ordered fold.
 //
-// One CTA owns one reduction block (block_size consecutive elements, the
-// ReductionPlan granularity of vecops.py:89-109).  The block partial is
-// v[0] + PW(v[1:]) in numpy's exact pairwise order (zk_plan.h).  Each
-// (leaf, lane) pair of the plan is one work item; the lane's elements are
-// leaf_start + lanes*g + q, exactly the elements numpy's lane accumulator q
-// visits, so the accumulation order matches bit for bit.  The element
-// callback computes the element's reduction term(s) AND performs any fused
-// elementwise update for that element (each element is visited exactly
-// once), which is how the BiCGStab kernels fold axpy/scale work into the
-// following dot product in a single HBM pass.
+// One CTA (or the consumer warps of one CTA) owns one reduction block
+// (block_size consecutive elements, the ReductionPlan granularity of
+// vecops.py:89-109).  The block partial is v[0] + PW(v[1:]) in numpy's exact
+// pairwise order (zk_plan.h).  Each (leaf, lane) pair of the plan is one work
+// item; the lane's elements are leaf_start + lanes*g + q, exactly the
+// elements numpy's lane accumulator q visits, so the accumulation order is
+// bit-identical.
+//
+// Element work is an `Op` with two steps so loads can run ahead of the
+// in-order accumulation:  `Item load(e)` issues the global loads for element
+// e, `apply(e, item, v)` performs the fused elementwise update for e (each
+// element is visited exactly once) and returns its reduction term(s).  A
+// lane prefetches Op::U elements before applying them in order, which keeps
+// U x (bytes per element) in flight per thread -- the block pass is an HBM
+// stream, and without this it is latency-bound.
 //
 // Block partials are folded left to right (vecops.py:159-161) by the CTA
 // that finishes last (threadfence + arrival counter), staged through shared
 // memory so the serial chain runs at DADD latency.
 #pragma once
 #include "zk_common.cuh"
+#include "zk_pipe.cuh"
 #include "zk_plan.h"
 
 namespace zk {
@@ -49,16 +55,17 @@ struct PlanPtrs {
 
 __device__ __forceinline__ const PlanHeader* plan_hdr(const char* p) { return reinterpret_cast<const PlanHeader*>(p); }
 
-// Runs the block pass for segment base `seg0` (global index of v[1]) using
-// plan `plan`.  `f(e, v)` fills v[NACC] for element e.  On return (after a
-// __syncthreads) nodes[root*NACC + a] holds PW of the segment for each
-// accumulator (when L > 0).  `nodes` is shared memory of nnodes*NACC values.
-template <typename V, int NACC, class F>
-__device__ __forceinline__ void block_pass(const char* plan, int64_t seg0, F& f, V* nodes) {
-    const PlanHeader* h = plan_hdr(plan);
+// Block pass over segment base `seg0` (global index of v[1]).  On return
+// (after a barrier) nodes[root*NACC + a] holds PW of the segment.
+template <typename V, int NACC, class Op, class Sync>
+__device__ __forceinline__ void block_pass(const char* plan, int64_t seg0, const Op& op, V* nodes, Sync sync) {
+    using Item = typename Op::Item;
     constexpr int LANES = VT<V>::lanes;
+    constexpr int U = Op::U;
+    const PlanHeader* h = plan_hdr(plan);
     const int L = h->L;
-    if (L > 0) {
+    const int nthr = sync.nthreads();
+    if (L > 0 && (int)threadIdx.x < nthr) {
         if (h->seq) {
             if (threadIdx.x == 0) {
                 V s[NACC];
@@ -66,7 +73,8 @@ __device__ __forceinline__ void block_pass(const char* plan, int64_t seg0, F& f,
                 for (int a = 0; a < NACC; ++a) s[a] = VT<V>::negzero();
                 for (int k = 0; k < L; ++k) {
                     V v[NACC];
-                    f(seg0 + k, v);
+                    Item it = op.load(seg0 + k);
+                    op.apply(seg0 + k, it, v);
 #pragma unroll
                     for (int a = 0; a < NACC; ++a) s[a] = VT<V>::add(s[a], v[a]);
                 }
@@ -78,26 +86,37 @@ __device__ __forceinline__ void block_pass(const char* plan, int64_t seg0, F& f,
             const int nitems = h->nleaves * LANES;
             const int lane = threadIdx.x & 31;
             const int q = lane & (LANES - 1);
-            for (int it0 = (threadIdx.x & ~31); it0 < nitems; it0 += blockDim.x) {
-                const int it = it0 + lane;
-                const bool valid = it < nitems;
-                const int leaf = it / LANES;
-                int2 lf = valid ? leaves[leaf] : make_int2(0, 0);
+            for (int it0 = (threadIdx.x & ~31); it0 < nitems; it0 += nthr) {
+                const int itm = it0 + lane;
+                const bool valid = itm < nitems;
+                const int leaf = itm / LANES;
+                const int2 lf = valid ? leaves[leaf] : make_int2(0, 0);
                 const int G = lf.y / LANES;
                 const int rem = lf.y - G * LANES;
+                const int64_t e0 = seg0 + lf.x + q;
+                const int64_t el = seg0 + lf.x + (int64_t)LANES * G + q;
+                const bool has_left = valid && q < rem;
+                Item left_item;
+                if (has_left) left_item = op.load(el);
                 V acc[NACC];
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) acc[a] = VT<V>::zero();
                 if (valid) {
-                    const int64_t e0 = seg0 + lf.x + q;
-                    f(e0, acc);
-                    for (int g = 1; g < G; ++g) {
-                        V v[NACC];
-                        f(e0 + (int64_t)LANES * g, v);
+                    for (int g0 = 0; g0 < G; g0 += U) {
+                        Item items[U];
 #pragma unroll
-                        for (int a = 0; a < NACC; ++a) acc[a] = VT<V>::add(acc[a], v[a]);
+                        for (int u = 0; u < U; ++u)
+                            if (g0 + u < G) items[u] = op.load(e0 + (int64_t)LANES * (g0 + u));
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (g0 + u < G) {
+                                V v[NACC];
+                                op.apply(e0 + (int64_t)LANES * (g0 + u), items[u], v);
+#pragma unroll
+                                for (int a = 0; a < NACC; ++a) acc[a] = (g0 + u == 0) ? v[a] : VT<V>::add(acc[a], v[a]);
+                            }
+                        }
                     }
-                } else {
-#pragma unroll
-                    for (int a = 0; a < NACC; ++a) acc[a] = VT<V>::zero();
                 }
                 // lane tree: (l0+l1)+(l2+l3) [+ ((l4+l5)+(l6+l7)) for real]
 #pragma unroll
@@ -110,8 +129,8 @@ __device__ __forceinline__ void block_pass(const char* plan, int64_t seg0, F& f,
                 }
                 // leftover elements, owned by lanes q < rem, added in order by lane 0
                 V left[NACC];
-                if (valid && q < rem) {
-                    f(seg0 + lf.x + (int64_t)LANES * G + q, left);
+                if (has_left) {
+                    op.apply(el, left_item, left);
                 } else {
 #pragma unroll
                     for (int a = 0; a < NACC; ++a) left[a] = VT<V>::zero();
@@ -132,67 +151,73 @@ __device__ __forceinline__ void block_pass(const char* plan, int64_t seg0, F& f,
             }
         }
     }
-    __syncthreads();
+    sync();
     if (L > 0 && !h->seq) {
         const int4* ops = reinterpret_cast<const int4*>(plan + h->ops_off);
         for (int r = 0; r < h->nrounds; ++r) {
             const int lo = h->round_off[r], hi = h->round_off[r + 1];
-            for (int o = lo + (int)threadIdx.x; o < hi; o += blockDim.x) {
-                int4 op = ops[o];
+            for (int o = lo + (int)threadIdx.x; o < hi; o += nthr) {
+                int4 opn = ops[o];
 #pragma unroll
                 for (int a = 0; a < NACC; ++a)
-                    nodes[op.x * NACC + a] = VT<V>::add(nodes[op.y * NACC + a], nodes[op.z * NACC + a]);
+                    nodes[opn.x * NACC + a] = VT<V>::add(nodes[opn.y * NACC + a], nodes[opn.z * NACC + a]);
             }
-            __syncthreads();
+            sync();
         }
     }
 }
 
-// Full segment reduction for block `blk` of a vector of length n.
-// Thread 0 returns the block partials in `out`; the elementwise callback is
-// invoked exactly once for every element of the block.
-template <typename V, int NACC, class F>
-__device__ __forceinline__ void block_reduce(PlanPtrs plans, int64_t n, int64_t block_size, int64_t blk, F& f,
-                                             V* nodes, V (&out)[NACC]) {
+// Full segment reduction for block `blk` of a vector of length n.  Thread 0
+// returns the block partials in `out`; op.apply runs exactly once per element.
+template <typename V, int NACC, class Op, class Sync = CtaSync>
+__device__ __forceinline__ void block_reduce(PlanPtrs plans, int64_t n, int64_t block_size, int64_t blk, const Op& op,
+                                             V* nodes, V (&out)[NACC], Sync sync = Sync()) {
     const int64_t base = blk * block_size;
     const bool full = base + block_size <= n;
     const char* plan = full ? plans.full : plans.tail;
     V v0[NACC];
-    if (threadIdx.x == 0) f(base, v0);
-    block_pass<V, NACC>(plan, base + 1, f, nodes);
+    if (threadIdx.x == 0) {
+        typename Op::Item it = op.load(base);
+        op.apply(base, it, v0);
+    }
+    block_pass<V, NACC>(plan, base + 1, op, nodes, sync);
     if (threadIdx.x == 0) {
         const PlanHeader* h = plan_hdr(plan);
 #pragma unroll
         for (int a = 0; a < NACC; ++a)
             out[a] = (h->L > 0) ? VT<V>::add(v0[a], nodes[h->root * NACC + a]) : v0[a];
     }
-    __syncthreads();  // nodes may be reused by the caller's next pass
+    sync();  // nodes may be reused by the caller's next pass
 }
 
-// Arrival counter: returns true in every thread of the CTA that arrives
-// last.  Thread 0 must have written this CTA's partials before the call.
-__device__ __forceinline__ bool arrive_last(unsigned int* counter, unsigned int nblocks) {
-    __shared__ unsigned int s_last;
+// Arrival counter over `total` arrivals (one per block): true in every
+// participating thread of the CTA making the last arrival.  Thread 0 must
+// have written this block's partials before the call.
+template <class Sync = CtaSync>
+__device__ __forceinline__ bool arrive_last(unsigned int* counter, unsigned int total, unsigned int* flag_smem,
+                                            Sync sync = Sync()) {
     __threadfence();
-    __syncthreads();
+    sync();
     if (threadIdx.x == 0) {
         unsigned int prev = atomicAdd(counter, 1u);
-        s_last = (prev == nblocks - 1) ? 1u : 0u;
+        *flag_smem = (prev == total - 1) ? 1u : 0u;
     }
-    __syncthreads();
-    if (s_last) __threadfence();
-    return s_last != 0;
+    sync();
+    const bool last = *flag_smem != 0;
+    if (last) __threadfence();
+    return last;
 }
 
 // Left fold of nacc interleaved partial streams (partials[b*nacc + a]),
 // vecops.py:159-161: total = p[0]; total = total + p[b] for b = 1..nb-1.
 // Componentwise Python adds are independent chains, so each real component
-// of each accumulator folds on its own warp.  `scratch` is shared memory of
-// at least `chunk * nacc` values.  Result valid in thread 0 (all threads
-// must call).
-template <typename V>
-__device__ void ordered_fold(const V* partials, int nacc, int64_t nb, V* scratch, int64_t chunk, V* result) {
-    constexpr int NC = sizeof(V) / sizeof(double);  // real components per value
+// of each accumulator folds on its own warp.  `scratch` holds at least
+// chunk*nacc values; `res_smem` >= 16 doubles.  Result valid in thread 0.
+template <typename V, class Sync = CtaSync>
+__device__ void ordered_fold(const V* partials, int nacc, int64_t nb, V* scratch, int64_t chunk, V* result,
+                             double* res_smem, Sync sync = Sync()) {
+    constexpr int NC = sizeof(V) / sizeof(double);
+    const int nthr = sync.nthreads();
     const int nchains = nacc * NC;
     const int warp = threadIdx.x >> 5;
     const bool chain = (threadIdx.x & 31) == 0 && warp < nchains;
@@ -202,25 +227,27 @@ __device__ void ordered_fold(const V* partials, int nacc, int64_t nb, V* scratch
     for (int64_t c0 = 0; c0 < nb; c0 += chunk) {
         const int64_t cn = (nb - c0 < chunk) ? nb - c0 : chunk;
         const int64_t nv = cn * nacc;
-        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) scratch[i] = __ldcg(partials + c0 * nacc + i);
-        __syncthreads();
+        if ((int)threadIdx.x < nthr)
+            for (int64_t i = threadIdx.x; i < nv; i += nthr) scratch[i] = __ldcg(partials + c0 * nacc + i);
+        sync();
         if (chain) {
             int64_t b = 0;
-            if (c0 == 0) { tot = sd[(0 * nacc + a) * NC + comp]; b = 1; }
+            if (c0 == 0) {
+                tot = sd[(0 * nacc + a) * NC + comp];
+                b = 1;
+            }
 #pragma unroll 16
             for (; b < cn; ++b) tot = __dadd_rn(tot, sd[(b * nacc + a) * NC + comp]);
         }
-        __syncthreads();
+        sync();
     }
-    // gather chain results in thread 0
-    __shared__ double s_res[16];
-    if (chain) s_res[warp] = tot;
-    __syncthreads();
+    if (chain) res_smem[warp] = tot;
+    sync();
     if (threadIdx.x == 0) {
         double* r = reinterpret_cast<double*>(result);
-        for (int c = 0; c < nchains; ++c) r[c] = s_res[c];
+        for (int c = 0; c < nchains; ++c) r[c] = res_smem[c];
     }
-    __syncthreads();
+    sync();
 }
 
 }  // namespace zk

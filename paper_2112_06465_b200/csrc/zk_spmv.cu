@@ -8,7 +8,9 @@
 
 namespace zk {
 
-SellView sell_view(const zk_csr* A, const zk_context* c) {
+// Ring geometry for a launch that also needs `extra` bytes of dynamic
+// shared memory after the ring (epilogue stash, reduction nodes).
+SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
     SellView v;
     v.n_rows = A->n_rows;
     v.n_cols = A->n_cols;
@@ -23,9 +25,26 @@ SellView sell_view(const zk_csr* A, const zk_context* c) {
     v.long_ia = A->long_ia;
     v.long_ja = A->long_ja;
     v.long_aa = A->long_aa;
+    const int w = A->wmax > 0 ? A->wmax : 1;
+    v.ja_off = 32 * w * 16;
+    v.stage_bytes = (32 * w * 20 + 127) / 128 * 128;
+    const long avail = (long)kSmemLimit - 1024 - kBarBytes - (long)extra;
+    int ns = (int)(avail / v.stage_bytes);
+    ns = ns > kMaxStages ? kMaxStages : (ns < 1 ? 1 : ns);
+    v.cw = ns < kConsumerWarps ? ns : kConsumerWarps;
+    v.ns = ns / v.cw * v.cw;
     v.swap = (A->nnz * 16 >= c->elide_bytes);
     v.fma = c->fma != 0;
     return v;
+}
+
+size_t pipe_smem_bytes(const SellView& v, size_t extra) {
+    return (size_t)kBarBytes + (size_t)v.ns * v.stage_bytes + extra;
+}
+
+unsigned pipe_grid(const zk_csr* A) {
+    int64_t g = A->nblocks < num_sms() ? A->nblocks : num_sms();
+    return (unsigned)(g > 0 ? g : 1);
 }
 
 namespace {
@@ -71,9 +90,17 @@ __global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __
     if (!ok) atomicOr(bad, 1u);
 }
 
-__global__ void __launch_bounds__(kThreads) k_spmv(SellView A, const double2* __restrict__ x, double2* __restrict__ y) {
-    auto epi = [&](int64_t row, double2 v) { y[row] = v; };
-    spmv_block(A, x, blockIdx.x, epi);
+struct PlainSpmv {
+    double2* __restrict__ y;
+    __device__ __forceinline__ void row(int64_t r, double2 v) { y[r] = v; }
+    __device__ __forceinline__ void block_done(int64_t) {}
+};
+
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv(SellView A, const double2* __restrict__ x,
+                                                          double2* __restrict__ y) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    PlainSpmv body{y};
+    sell_pipeline(A, x, body, smem);
 }
 
 template <class T>
@@ -128,6 +155,8 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
         slice_off[s + 1] = slice_off[s] + (int64_t)kSlice * w;
     }
     for (int64_t b = 0; b < A->nblocks; ++b) long_blk_ptr[b + 1] += long_blk_ptr[b];
+    for (int64_t s = 0; s < A->nslices; ++s)
+        A->wmax = std::max<int32_t>(A->wmax, (int32_t)((slice_off[s + 1] - slice_off[s]) / kSlice));
     A->sell_elems = slice_off[A->nslices];
     A->n_long = (int32_t)long_row.size();
     cudaStream_t st = c->stream;
@@ -181,8 +210,10 @@ void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
         ZK_CUDA(cudaMemsetAsync(y, 0, sizeof(double2) * A->n_rows, c->stream));
         return;
     }
-    SellView v = sell_view(A, c);
-    k_spmv<<<(unsigned)A->nblocks, kThreads, 0, c->stream>>>(v, x, y);
+    SellView v = sell_view(A, c, 0);
+    const size_t smem = pipe_smem_bytes(v, 0);
+    ZK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_spmv<<<pipe_grid(A), kPipeThreads, smem, c->stream>>>(v, x, y);
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }

@@ -153,3 +153,42 @@ def test_solver_reuse_and_determinism(bicgstab_golden):
     r2 = _solve_golden(g)
     assert r1[1].residual_history == r2[1].residual_history
     assert bits(r1[0].data) == bits(r2[0].data)
+
+
+def _wide_dominant(n, lo, hi, seed):
+    """Diagonally dominant matrix with lo..hi entries per row (wide SELL
+    slices: few ring stages, so stages are reused within and across blocks)."""
+    rng = np.random.default_rng(seed)
+    lens = rng.integers(lo, hi + 1, n)
+    ia = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=ia[1:])
+    rows, cols, vals = [], [], []
+    for i, k in enumerate(lens):
+        c = np.sort(rng.choice(np.setdiff1d(np.arange(max(0, i - 200), min(n, i + 200)), [i]), k - 1, replace=False))
+        c = np.sort(np.append(c, i))
+        v = rng.standard_normal(k) + 1j * rng.standard_normal(k)
+        v[c == i] = (np.abs(v).sum() + 2.0) * np.exp(1j * rng.uniform(-0.4, 0.4))
+        cols.append(c)
+        vals.append(v)
+    ja = np.concatenate(cols).astype(np.int64)
+    aa = np.concatenate(vals)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    return ia, ja, aa, b
+
+
+@pytest.mark.parametrize("n,lo,hi", [(200, 30, 45), (9000, 40, 65), (13000, 60, 65)])
+def test_wide_rows_stage_reuse(n, lo, hi):
+    """Regression: ring stages shared by several consumer warps raced (the
+    mbarrier parity wait cannot tell use u from use u+2)."""
+    ia, ja, aa, b = _wide_dominant(n, lo, hi, seed=n)
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for _ in range(3):
+        assert bits(Z.spmv(A, Z.ZVector(x)).data) == bits(O.spmv(n, n, ia, ja, aa, x))
+    M = Z.build_jacobi(A)
+    xo, hist, it, st, _ = O.bicgstab(n, ia, ja, aa, b, M.data, None, 1e-10, 500)
+    for _ in range(3):
+        xs, rep = Z.solve_bicgstab(A, Z.ZVector(b), M, Z.SolverConfig(tolerance=1e-10, max_iterations=500))
+        assert rep.residual_history == hist
+        assert bits(xs.data) == bits(xo)
