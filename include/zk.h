@@ -91,8 +91,8 @@ zk_status zk_event_elapsed(zk_context* ctx, int start_slot, int stop_slot, doubl
  * the host and brackets every phase kernel with CUDA events; zk_profile_read
  * returns the accumulated device time and launch count per phase, in this
  * order: setup, p_first, spmv_pivot, s_update, x_alpha, true_res_s, spmv_t,
- * xr_update, true_res_p. */
-#define ZK_NPHASES 9
+ * xr_update, p_next, true_res. */
+#define ZK_NPHASES 10
 zk_status zk_profile_enable(zk_context* ctx, int on);
 zk_status zk_profile_read(zk_context* ctx, double* total_ms, int64_t* launches);
 

@@ -185,7 +185,7 @@ def launch_count() -> int:
 
 
 PHASES = ("setup", "p_first", "spmv_pivot", "s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update",
-          "true_res_p")
+          "p_next", "true_res")
 
 
 def event_record(slot: int) -> None:

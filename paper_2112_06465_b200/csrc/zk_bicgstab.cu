@@ -27,6 +27,7 @@
 #include <cstring>
 
 #include "zk_internal.h"
+#include "zk_blockred.cuh"
 #include "zk_spmv.cuh"
 
 namespace zk {
@@ -58,9 +59,11 @@ struct SolverBufs {
 
 constexpr int kStashC = kBlock * sizeof(double2);  // 64 KiB complex stash
 constexpr int kStashR = kBlock * sizeof(double);   // 32 KiB real stash
-constexpr int kNodeBytes = 8 * 1024;               // plan nodes (<= 129 nodes x 2 acc x 16 B)
+constexpr int kNodesPerBuf = 2 * 136;             // node slots per buffer (<= 129 nodes x NACC 2)
+constexpr int kNodeBytes = 2 * kNodesPerBuf * 16;  // double-buffered plan nodes
 constexpr int kRedThreads = 288;                   // 65 complex leaves x 4 lanes fit one pass
-constexpr int kEwSmem = 32 * 1024 + kNodeBytes;    // fold scratch (2048 x 16 B) + nodes
+constexpr int kFoldScratch = 8 * 1024;             // warp_fold staging in the level-1 kernels
+constexpr int kEwSmem = kFoldScratch + kNodeBytes;
 
 struct SolverPlan {
     int64_t n = 0;
@@ -82,18 +85,6 @@ __device__ __forceinline__ void stop(SolverState* st, int32_t status, int32_t wh
     st->status = status;
     st->what = what;
     st->done = 1;
-}
-
-// p = ((p + F1(-w, v)) * beta) + F1(1, r); p^ = F1(p, minv)
-// (krylov.py:263-266: zaxpy, zscal, zaxpy, M.apply -- separate roundings).
-__device__ __forceinline__ void p_update(const SolverBufs& B, double2 mw, double2 beta, int64_t i) {
-    const bool fma = B.fma;
-    double2 p = B.p[i];
-    p = cadd(p, f1(mw, B.v[i], fma));
-    p = f1(p, beta, fma);
-    p = cadd(p, f1(make_double2(1.0, 0.0), B.r[i], fma));
-    B.p[i] = p;
-    if (B.jacobi) B.ph[i] = f1(p, __ldg(B.minv + i), fma);
 }
 
 // Reduction ops over the stash of the block just computed (smem reads only).
@@ -123,45 +114,86 @@ struct StashSelfDot {  // <r0, r0> (setup)
     }
 };
 
-struct StashDot {  // <rs, stash> (pivot)
-    const double2* rs;
-    const double2* stash;
-    int64_t base;
-    bool fma;
-    struct Item { double2 r; };
-    static constexpr int U = 4;
-    __device__ Item load(int64_t e) const { return {__ldg(rs + e)}; }
-    __device__ void apply(int64_t e, const Item& it, double2 (&v)[1]) const {
-        v[0] = f1(conjz(it.r), stash[e - base], fma);
-    }
-};
 
-struct StashTT {  // <t, t>, <t, s>
-    const double2* s;
-    const double2* stash;
+// Reduction ops over a shared-memory stash ring of per-row terms.
+template <typename V, int NACC>
+struct StashOp {
+    const V* stash;  // element e of the block at ((e - base) & mask) * NACC
     int64_t base;
-    bool fma;
-    struct Item { double2 s; };
-    static constexpr int U = 4;
-    __device__ Item load(int64_t e) const { return {s[e]}; }
-    __device__ void apply(int64_t e, const Item& it, double2 (&v)[2]) const {
-        double2 t = stash[e - base];
-        double2 ct = conjz(t);
-        v[0] = f1(ct, t, fma);
-        v[1] = f1(ct, it.s, fma);
-    }
-};
-
-struct StashReal {  // stashed |res|^2
-    const double* stash;
-    int64_t base;
+    int mask;
     struct Item {};
     static constexpr int U = 1;
     __device__ Item load(int64_t) const { return {}; }
-    __device__ void apply(int64_t e, const Item&, double (&v)[1]) const { v[0] = stash[e - base]; }
+    __device__ void apply(int64_t e, const Item&, V (&v)[NACC]) const {
+        const int64_t k = (e - base) & mask;
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) v[a] = stash[k * NACC + a];
+    }
+};
+
+// Windowed block reduction for the SpMV-phase kernels.  Rows deposit their
+// reduction terms in a stash ring; after every window (named barrier passed)
+// the leaves lying entirely in finished rows are summed (leaf_upto table),
+// and after the last one warp 0 combines the tree and finishes the block
+// while the other warps go on.  Per thread state; every consumer thread
+// makes the same calls.
+template <typename V, int NACC>
+struct WinRed {
+    const char* plan_full;
+    const char* plan_tail;
+    V* stash;
+    int mask;   // stash rows - 1
+    V* nodes;   // 2 buffers of kNodesPerBuf
+    int buf;
+    int done;   // leaves already summed for the current block
+    bool got_v0;
+    V v0[NACC];
+
+    __device__ __forceinline__ const char* plan(int64_t base, int64_t n) const {
+        return base + kBlock <= n ? plan_full : plan_tail;
+    }
+    __device__ __forceinline__ void put(int64_t row, const V (&val)[NACC]) {
+        const int64_t k = row & (kBlock - 1) & mask;
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) stash[k * NACC + a] = val[a];
+    }
+    __device__ __forceinline__ void take_v0() {
+        if (!got_v0 && threadIdx.x == 0) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) v0[a] = stash[a];
+        }
+        got_v0 = true;
+    }
+    __device__ __forceinline__ void window(int64_t blk, int64_t n, int slices_done) {
+        const int64_t base = blk * kBlock;
+        const char* p = plan(base, n);
+        take_v0();
+        const int hi = plan_hdr(p)->leaf_upto[slices_done];
+        leaf_phase<V, NACC>(p, base + 1, StashOp<V, NACC>{stash, base, mask}, nodes + buf * kNodesPerBuf,
+                            kConsumers, done, hi);
+        done = hi;
+    }
+    // Returns true in warp 0 of the CTA that finished the last block.
+    __device__ __forceinline__ bool finish(int64_t blk, int64_t n, V* partials, unsigned int* counter,
+                                           unsigned int total) {
+        const int64_t base = blk * kBlock;
+        const char* p = plan(base, n);
+        take_v0();
+        V* nb = nodes + buf * kNodesPerBuf;
+        leaf_phase<V, NACC>(p, base + 1, StashOp<V, NACC>{stash, base, mask}, nb, kConsumers, done);
+        done = 0;
+        got_v0 = false;
+        buf ^= 1;
+        named_sync(1, kConsumers);
+        if ((threadIdx.x >> 5) != 0) return false;
+        V pw[NACC];
+        warp_tree<V, NACC>(p, nb, pw);
+        return warp_finish<V, NACC>(p, v0, pw, partials, blk, counter, total);
+    }
 };
 
 // ---- setup: r0 = b - A x0, ||b||, ||r0||, <r0, r0> (krylov.py:159-168, 255) ----
+// Runs once per solve; uses the plain (CTA-wide) block reduction.
 struct SetupBody {
     SolverBufs B;
     PlanPtrs pc, pr;
@@ -169,13 +201,16 @@ struct SetupBody {
     char* nodes;
     unsigned int* flag;
     double* res;
-    __device__ void row(int64_t row, double2 ax) {
+    struct RowCtx { double2 b; };
+    __device__ RowCtx prefetch(int64_t row) { return {B.b[row]}; }
+    __device__ void row(int64_t row, double2 ax, const RowCtx& c) {
         const int64_t base = (row / kBlock) * kBlock;
-        double2 r0 = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, B.fma));
+        double2 r0 = cadd(c.b, f1(make_double2(-1.0, 0.0), ax, B.fma));
         B.r[row] = r0;
         B.rs[row] = r0;
         stash[row - base] = r0;
     }
+    __device__ void window_done(int64_t, int) {}
     __device__ void block_done(int64_t blk) {
         const int64_t base = blk * kBlock;
         double outr[2];
@@ -236,39 +271,59 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_setup(SellView A, SolverBuf
     sell_pipeline(A, B.x, body, smem);
 }
 
+__device__ __forceinline__ int stash_rows(const SellView& A) { return A.win < kBlock / kSlice ? kStashRows : kBlock; }
+
 // ---- K1: p update for the first iteration (p = v = 0) ----
+// p = ((p + F1(-w, v)) * beta) + F1(1, r); p^ = F1(p, minv)
+// (krylov.py:263-266: zaxpy, zscal, zaxpy, M.apply -- separate roundings).
+__device__ __forceinline__ void p_update(const SolverBufs& B, double2 mw, double2 beta, int64_t i, double2 p,
+                                         double2 v, double2 r, double2 m) {
+    const bool fma = B.fma;
+    p = cadd(p, f1(mw, v, fma));
+    p = f1(p, beta, fma);
+    p = cadd(p, f1(make_double2(1.0, 0.0), r, fma));
+    B.p[i] = p;
+    if (B.jacobi) B.ph[i] = f1(p, m, fma);
+}
+
 __global__ void __launch_bounds__(256) k_p_first(SolverBufs B) {
     const SolverState* st = B.st;
     if (st->done) return;
     const double2 mw = neg(st->omega), beta = st->beta;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride) p_update(B, mw, beta, i);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride)
+        p_update(B, mw, beta, i, B.p[i], B.v[i], B.r[i], B.jacobi ? B.minv[i] : make_double2(0.0, 0.0));
+}
+
+// ---- Kp: next iteration's p update (after K5 has formed r and beta) ----
+__global__ void __launch_bounds__(256) k_p_next(SolverBufs B) {
+    const SolverState* st = B.st;
+    if (st->done) return;
+    const double2 mw = neg(st->omega), beta = st->beta;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride)
+        p_update(B, mw, beta, i, B.p[i], B.v[i], B.r[i], B.jacobi ? __ldg(B.minv + i) : make_double2(0.0, 0.0));
 }
 
 // ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
 struct PivotBody {
     SolverBufs B;
-    PlanPtrs pc;
-    double2* stash;
-    char* nodes;
-    unsigned int* flag;
-    double* res;
-    __device__ void row(int64_t row, double2 av) {
+    WinRed<double2, 1> red;
+    struct RowCtx { double2 rs; };
+    __device__ RowCtx prefetch(int64_t row) { return {__ldg(B.rs + row)}; }
+    __device__ void row(int64_t row, double2 av, const RowCtx& c) {
         B.v[row] = av;
-        stash[row - (row / kBlock) * kBlock] = av;
+        const double2 t[1] = {f1(conjz(c.rs), av, B.fma)};
+        red.put(row, t);
     }
+    __device__ void window_done(int64_t blk, int j) { red.window(blk, B.n, j); }
     __device__ void block_done(int64_t blk) {
-        const int64_t base = blk * kBlock;
-        double2 out[1];
-        block_reduce<double2, 1>(pc, B.n, kBlock, blk, StashDot{B.rs, stash, base, B.fma},
-                                 reinterpret_cast<double2*>(nodes), out, Sync());
         double2* PC = reinterpret_cast<double2*>(B.partials);
-        if (threadIdx.x == 0) PC[blk] = out[0];
-        SolverState* st = B.st;
-        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
+        if (!red.finish(blk, B.n, PC, &B.st->counter, (unsigned)B.nblocks)) return;
         double2 pivot;
-        ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &pivot, res, Sync());
-        if (threadIdx.x != 0) return;
+        warp_fold<double2>(PC, 1, B.nblocks, red.stash, 1024, &pivot);
+        if ((threadIdx.x & 31) != 0) return;
+        SolverState* st = B.st;
         st->counter = 0;
         if (small_py(pivot)) {
             stop(st, ST_BREAKDOWN, BD_PIVOT);
@@ -280,103 +335,79 @@ struct PivotBody {
 
 __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_pivot(SellView A, SolverBufs B, PlanPtrs pc) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;
     if (st->done) return;
     unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    PivotBody body{B, pc, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag,
-                   s_res};
+    const int rows = stash_rows(A);
+    PivotBody body{B, {pc.full, pc.tail, reinterpret_cast<double2*>(extra), rows - 1,
+                       reinterpret_cast<double2*>(extra + rows * sizeof(double2)), 0, 0, false, {}}};
     sell_pipeline(A, B.ph, body, smem);
 }
 
-// ---- K3: s = r + F1(-alpha, v); s^ = M s; ||s|| -> s-check (krylov.py:272-275) ----
-struct SUpdateOp {
-    const double2* r;
-    const double2* v;
-    const double2* minv;
-    double2* s;
-    double2* sh;
-    double2 ma;
-    bool jacobi, fma;
-    struct Item { double2 r, v, m; };
-    static constexpr int U = 4;
-    __device__ Item load(int64_t e) const {
-        Item it;
-        it.r = r[e];
-        it.v = v[e];
-        if (jacobi) it.m = __ldg(minv + e);
-        return it;
+// ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
+struct TBody {
+    SolverBufs B;
+    WinRed<double2, 2> red;
+    struct RowCtx { double2 s; };
+    __device__ RowCtx prefetch(int64_t row) { return {B.s[row]}; }
+    __device__ void row(int64_t row, double2 at, const RowCtx& c) {
+        B.t[row] = at;
+        const double2 ct = conjz(at);
+        const double2 t[2] = {f1(ct, at, B.fma), f1(ct, c.s, B.fma)};
+        red.put(row, t);
     }
-    __device__ void apply(int64_t e, const Item& it, double (&out)[1]) const {
-        double2 sv = cadd(it.r, f1(ma, it.v, fma));
-        s[e] = sv;
-        if (jacobi) sh[e] = f1(sv, it.m, fma);
-        out[0] = abs2_np(sv);
+    __device__ void window_done(int64_t blk, int j) { red.window(blk, B.n, j); }
+    __device__ void block_done(int64_t blk) {
+        double2* PC = reinterpret_cast<double2*>(B.partials);
+        if (!red.finish(blk, B.n, PC, &B.st->counter, (unsigned)B.nblocks)) return;
+        double2 tot[2];
+        warp_fold<double2>(PC, 2, B.nblocks, red.stash, 1024, tot);
+        if ((threadIdx.x & 31) != 0) return;
+        SolverState* st = B.st;
+        st->counter = 0;
+        if (small_py(tot[0])) {
+            stop(st, ST_BREAKDOWN, BD_TT);
+            return;
+        }
+        const double2 w = cdiv_py(tot[1], tot[0]);
+        st->omega = w;
+        if (small_py(w)) stop(st, ST_BREAKDOWN, BD_OMEGA);
     }
 };
 
-__global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_t(SellView A, SolverBufs B, PlanPtrs pc) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
-    SolverState* st = B.st;
-    if (st->done) return;
-    const int64_t blk = blockIdx.x;
-    SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
-    double out[1];
-    block_reduce<double, 1>(pr, B.n, kBlock, blk, op, reinterpret_cast<double*>(smem + 32 * 1024), out);
-    if (threadIdx.x == 0) B.partials[blk] = out[0];
-    if (!arrive_last(&st->counter, gridDim.x, &s_flag)) return;
-    double ss;
-    ordered_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), 4096, &ss, s_res);
-    if (threadIdx.x != 0) return;
-    st->counter = 0;
-    st->scheck = (__ddiv_rn(__dsqrt_rn(ss), st->b_norm) <= st->tol) ? 1 : 0;
-}
-
-// ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
-__global__ void __launch_bounds__(256) k_x_alpha(SolverBufs B) {
-    SolverState* st = B.st;
-    if (st->done || !st->scheck) return;
-    const double2 a = st->alpha;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride)
-        B.x[i] = cadd(B.x[i], f1(a, B.ph[i], B.fma));
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha_applied = 1;
+    if (B.st->done) return;
+    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
+    const int rows = stash_rows(A);
+    TBody body{B, {pc.full, pc.tail, reinterpret_cast<double2*>(extra), rows - 1,
+                   reinterpret_cast<double2*>(extra + 2 * rows * sizeof(double2)), 0, 0, false, {}}};
+    sell_pipeline(A, B.sh, body, smem);
 }
 
 // ---- true residual ||b + F1(-1, A x)|| / ||b|| (krylov.py:183-186) ----
-// MODE 0: on the s-check path (K6x);  MODE 1: end of iteration (K61), fused
-// with the next iteration's p update.
+// MODE 0: on the s-check path (K6x);  MODE 1: end of iteration (K61).
 template <int MODE>
 struct ResBody {
     SolverBufs B;
-    PlanPtrs pr;
-    double* stash;
-    char* nodes;
-    unsigned int* flag;
-    double* res;
-    double2 mw, beta;
+    WinRed<double, 1> red;
     cudaGraphConditionalHandle cond;
     int use_cond;
-    __device__ void row(int64_t row, double2 ax) {
-        double2 rv = cadd(B.b[row], f1(make_double2(-1.0, 0.0), ax, B.fma));
-        stash[row - (row / kBlock) * kBlock] = abs2_np(rv);
-        if (MODE == 1) p_update(B, mw, beta, row);
+    struct RowCtx { double2 b; };
+    __device__ RowCtx prefetch(int64_t row) { return {B.b[row]}; }
+    __device__ void row(int64_t row, double2 ax, const RowCtx& c) {
+        const double2 rv = cadd(c.b, f1(make_double2(-1.0, 0.0), ax, B.fma));
+        const double t[1] = {abs2_np(rv)};
+        red.put(row, t);
     }
+    __device__ void window_done(int64_t blk, int j) { red.window(blk, B.n, j); }
     __device__ void block_done(int64_t blk) {
-        const int64_t base = blk * kBlock;
-        double out[1];
-        block_reduce<double, 1>(pr, B.n, kBlock, blk, StashReal{stash, base}, reinterpret_cast<double*>(nodes), out,
-                                Sync());
-        if (threadIdx.x == 0) B.partials[blk] = out[0];
-        SolverState* st = B.st;
-        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
+        if (!red.finish(blk, B.n, B.partials, &B.st->counter, (unsigned)B.nblocks)) return;
         double rr;
-        ordered_fold<double>(B.partials, 1, B.nblocks, stash, 4096, &rr, res, Sync());
-        if (threadIdx.x != 0) return;
+        warp_fold<double>(B.partials, 1, B.nblocks, red.stash, 2048, &rr);
+        if ((threadIdx.x & 31) != 0) return;
+        SolverState* st = B.st;
         st->counter = 0;
         const double rel = __ddiv_rn(__dsqrt_rn(rr), st->b_norm);
         if (MODE == 0) {
@@ -410,65 +441,97 @@ template <int MODE>
 __global__ void __launch_bounds__(kPipeThreads, 1) k_true_res(SellView A, SolverBufs B, PlanPtrs pr,
                                                               cudaGraphConditionalHandle cond, int use_cond) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (st->done || (MODE == 0 && !st->scheck)) {
         if (MODE == 1 && use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
         return;
     }
     unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    ResBody<MODE> body{B, pr, reinterpret_cast<double*>(extra), reinterpret_cast<char*>(extra + kStashR), &s_flag,
-                       s_res, neg(st->omega), st->beta, cond, use_cond};
+    const int rows = stash_rows(A);
+    ResBody<MODE> body{B, {pr.full, pr.tail, reinterpret_cast<double*>(extra), rows - 1,
+                           reinterpret_cast<double*>(extra + rows * sizeof(double)), 0, 0, false, {}},
+                       cond, use_cond};
     sell_pipeline(A, B.x, body, smem);
 }
 
-// ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
-struct TBody {
-    SolverBufs B;
-    PlanPtrs pc;
-    double2* stash;
-    char* nodes;
-    unsigned int* flag;
-    double* res;
-    __device__ void row(int64_t row, double2 at) {
-        B.t[row] = at;
-        stash[row - (row / kBlock) * kBlock] = at;
-    }
-    __device__ void block_done(int64_t blk) {
+// ---- persistent block-pass kernels for the fused level-1 phases ----------
+// One CTA loops over blocks; per block: leaf phase (all threads, operands
+// prefetched in registers), one CTA barrier, then warp 0 combines the tree
+// while the other warps start the next block.  Nodes are double-buffered.
+template <typename V, int NACC, class Op, class Done>
+__device__ __forceinline__ void persistent_blocks(PlanPtrs plans, int64_t n, int64_t nblocks, const Op& op,
+                                                  V* nodes, V* partials, unsigned int* counter, Done& done) {
+    int buf = 0;
+    for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
         const int64_t base = blk * kBlock;
-        double2 out[2];
-        block_reduce<double2, 2>(pc, B.n, kBlock, blk, StashTT{B.s, stash, base, B.fma},
-                                 reinterpret_cast<double2*>(nodes), out, Sync());
-        double2* PC = reinterpret_cast<double2*>(B.partials);
+        const char* plan = (base + kBlock <= n) ? plans.full : plans.tail;
+        V* nb = nodes + buf * kNodesPerBuf;
+        V v0[NACC];
         if (threadIdx.x == 0) {
-            PC[2 * blk] = out[0];
-            PC[2 * blk + 1] = out[1];
+            typename Op::Item it = op.load(base);
+            op.apply(base, it, v0);
         }
-        SolverState* st = B.st;
-        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
-        double2 tot[2];
-        ordered_fold<double2>(PC, 2, B.nblocks, stash, 2048, tot, res, Sync());
-        if (threadIdx.x != 0) return;
-        st->counter = 0;
-        if (small_py(tot[0])) {
-            stop(st, ST_BREAKDOWN, BD_TT);
-            return;
-        }
-        const double2 w = cdiv_py(tot[1], tot[0]);
-        st->omega = w;
-        if (small_py(w)) stop(st, ST_BREAKDOWN, BD_OMEGA);
+        leaf_phase<V, NACC>(plan, base + 1, op, nb, blockDim.x);
+        __syncthreads();
+        buf ^= 1;
+        if ((threadIdx.x >> 5) != 0) continue;
+        V pw[NACC];
+        warp_tree<V, NACC>(plan, nb, pw);
+        if (warp_finish<V, NACC>(plan, v0, pw, partials, blk, counter, (unsigned)nblocks)) done();
+    }
+}
+
+// ---- K3: s = r + F1(-alpha, v); s^ = M s; ||s|| -> s-check (krylov.py:272-275) ----
+struct SUpdateOp {
+    const double2* r;
+    const double2* v;
+    const double2* minv;
+    double2* s;
+    double2* sh;
+    double2 ma;
+    bool jacobi, fma;
+    struct Item { double2 r, v, m; };
+    static constexpr int U = 2;
+    __device__ Item load(int64_t e) const {
+        Item it;
+        it.r = r[e];
+        it.v = v[e];
+        if (jacobi) it.m = __ldg(minv + e);
+        return it;
+    }
+    __device__ void apply(int64_t e, const Item& it, double (&out)[1]) const {
+        double2 sv = cadd(it.r, f1(ma, it.v, fma));
+        s[e] = sv;
+        if (jacobi) sh[e] = f1(sv, it.m, fma);
+        out[0] = abs2_np(sv);
     }
 };
 
-__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_t(SellView A, SolverBufs B, PlanPtrs pc) {
+__global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
-    if (B.st->done) return;
-    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    TBody body{B, pc, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag, s_res};
-    sell_pipeline(A, B.sh, body, smem);
+    SolverState* st = B.st;
+    if (st->done) return;
+    SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
+    double* nodes = reinterpret_cast<double*>(smem + kFoldScratch);
+    auto done = [&]() {
+        double ss;
+        warp_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), kFoldScratch / 8, &ss);
+        if ((threadIdx.x & 31) != 0) return;
+        st->counter = 0;
+        st->scheck = (__ddiv_rn(__dsqrt_rn(ss), st->b_norm) <= st->tol) ? 1 : 0;
+    };
+    persistent_blocks<double, 1>(pr, B.n, B.nblocks, op, nodes, B.partials, &st->counter, done);
+}
+
+// ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
+__global__ void __launch_bounds__(256) k_x_alpha(SolverBufs B) {
+    SolverState* st = B.st;
+    if (st->done || !st->scheck) return;
+    const double2 a = st->alpha;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B.n; i += stride)
+        B.x[i] = cadd(B.x[i], f1(a, B.ph[i], B.fma));
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha_applied = 1;
 }
 
 // ---- K5: x, r updates and <r~, r> -> rho', beta (krylov.py:288-290, 255-261) ----
@@ -483,7 +546,7 @@ struct XrOp {
     double2 a, w, mw;
     bool applied, fma;
     struct Item { double2 x, ph, sh, s, t, rs; };
-    static constexpr int U = 2;
+    static constexpr int U = 1;
     __device__ Item load(int64_t e) const {
         Item it;
         it.x = x[e];
@@ -507,28 +570,25 @@ struct XrOp {
 
 __global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, PlanPtrs pc) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
     SolverState* st = B.st;
     if (st->done) return;
-    const int64_t blk = blockIdx.x;
     const double2 a = st->alpha, w = st->omega;
     XrOp op{B.x, B.r, B.ph, B.sh, B.s, B.t, B.rs, a, w, neg(w), st->alpha_applied != 0, B.fma};
-    double2 out[1];
-    block_reduce<double2, 1>(pc, B.n, kBlock, blk, op, reinterpret_cast<double2*>(smem + 32 * 1024), out);
+    double2* nodes = reinterpret_cast<double2*>(smem + kFoldScratch);
     double2* PC = reinterpret_cast<double2*>(B.partials);
-    if (threadIdx.x == 0) PC[blk] = out[0];
-    if (!arrive_last(&st->counter, gridDim.x, &s_flag)) return;
-    double2 rho_next;
-    ordered_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), 2048, &rho_next, s_res);
-    if (threadIdx.x != 0) return;
-    st->counter = 0;
-    const double2 rho = st->rho;
-    st->rho_old = rho;
-    st->rho = rho_next;
-    // beta for the next iteration (speculative: K61 stops before it is used
-    // if the loop ends, and breaks down on the same checks as krylov.py:256-259)
-    if (!small_py(rho) && !small_py(w)) st->beta = cmul_py(cdiv_py(rho_next, rho), cdiv_py(a, w));
+    auto done = [&]() {
+        double2 rho_next;
+        warp_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), kFoldScratch / 16, &rho_next);
+        if ((threadIdx.x & 31) != 0) return;
+        st->counter = 0;
+        const double2 rho = st->rho;
+        st->rho_old = rho;
+        st->rho = rho_next;
+        // beta for the next iteration (speculative: K61 stops before it is
+        // used if the loop ends, and breaks down on krylov.py:256-259's checks)
+        if (!small_py(rho) && !small_py(w)) st->beta = cmul_py(cdiv_py(rho_next, rho), cdiv_py(a, w));
+    };
+    persistent_blocks<double2, 1>(pc, B.n, B.nblocks, op, nodes, PC, &st->counter, done);
 }
 
 }  // namespace
@@ -543,16 +603,16 @@ void smem_attr(K kernel, size_t bytes) {
 struct Launch {
     zk_context* c;
     SolverPlan* P;
-    SellView Ac, Ar;        // ring geometry with a complex / real stash
-    size_t smem_c, smem_r;  // dynamic smem of the SpMV-phase kernels
+    SellView As, Ap, At, Ar;                // ring geometry of setup, K2, K4, K6x/K61 (their stashes differ)
+    size_t smem_s, smem_p, smem_t, smem_r;  // dynamic smem of the SpMV-phase kernels
     PlanPtrs pc, pr;
-    unsigned nb, ew, pg;
+    unsigned nb, ew, pg, rg;  // blocks, elementwise grid, SpMV grid, level-1 persistent grid
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
-// kernel and ev[k+1] after it (prologue phases 0-1, body phases 2-8).
+// kernel and ev[k+1] after it (prologue phases 0-1, body phases 2-9).
 struct PhaseEvents {
-    cudaEvent_t ev[10] = {};
+    cudaEvent_t ev[11] = {};
     bool on = false;
     void rec(int k, cudaStream_t s) {
         if (on) ZK_CUDA(cudaEventRecord(ev[k], s));
@@ -561,7 +621,7 @@ struct PhaseEvents {
 
 void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(0, s);
-    k_setup<<<L.pg, kPipeThreads, L.smem_c, s>>>(L.Ac, L.P->bufs, L.pc, L.pr);
+    k_setup<<<L.pg, kPipeThreads, L.smem_s, s>>>(L.As, L.P->bufs, L.pc, L.pr);
     if (pe) pe->rec(1, s);
     k_p_first<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(2, s);
@@ -570,22 +630,24 @@ void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr)
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(2, s);
-    k_spmv_pivot<<<L.pg, kPipeThreads, L.smem_c, s>>>(L.Ac, L.P->bufs, L.pc);
+    k_spmv_pivot<<<L.pg, kPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.pc);
     if (pe) pe->rec(3, s);
-    k_s_update<<<L.nb, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
+    k_s_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
     if (pe) pe->rec(4, s);
     k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(5, s);
     k_true_res<0><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, 0);
     if (pe) pe->rec(6, s);
-    k_spmv_t<<<L.pg, kPipeThreads, L.smem_c, s>>>(L.Ac, L.P->bufs, L.pc);
+    k_spmv_t<<<L.pg, kPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.pc);
     if (pe) pe->rec(7, s);
-    k_xr_update<<<L.nb, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
+    k_xr_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
     if (pe) pe->rec(8, s);
-    k_true_res<1><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, use_cond);
+    k_p_next<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(9, s);
+    k_true_res<1><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, use_cond);
+    if (pe) pe->rec(10, s);
 }
-constexpr int kBodyKernels = 7;
+constexpr int kBodyKernels = 8;
 
 void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
     ZK_CUDA(cudaEventSynchronize(pe.ev[last + 1]));
@@ -598,9 +660,9 @@ void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
 }
 
 void set_attrs(const Launch& L) {
-    smem_attr(k_setup, L.smem_c);
-    smem_attr(k_spmv_pivot, L.smem_c);
-    smem_attr(k_spmv_t, L.smem_c);
+    smem_attr(k_setup, L.smem_s);
+    smem_attr(k_spmv_pivot, L.smem_p);
+    smem_attr(k_spmv_t, L.smem_t);
     smem_attr(k_true_res<0>, L.smem_r);
     smem_attr(k_true_res<1>, L.smem_r);
     smem_attr(k_s_update, kEwSmem);
@@ -722,14 +784,24 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     Launch L;
     L.c = c;
     L.P = P;
-    L.Ac = sell_view(A, c, kStashC + kNodeBytes);
-    L.Ar = sell_view(A, c, kStashR + kNodeBytes);
-    L.smem_c = pipe_smem_bytes(L.Ac, kStashC + kNodeBytes);
-    L.smem_r = pipe_smem_bytes(L.Ar, kStashR + kNodeBytes);
+    // stash ring: kStashRows rows when the matrix has no long rows
+    // (windowed reductions), a whole 4096-row block otherwise
+    const size_t srows = A->n_long ? kBlock : kStashRows;
+    const size_t ex_p = srows * 16 + kNodeBytes, ex_t = 2 * srows * 16 + kNodeBytes, ex_r = srows * 8 + kNodeBytes;
+    L.As = sell_view(A, c, kStashC + kNodeBytes);
+    L.As.win = kBlock / kSlice;
+    L.Ap = sell_view(A, c, ex_p);
+    L.At = sell_view(A, c, ex_t);
+    L.Ar = sell_view(A, c, ex_r);
+    L.smem_s = pipe_smem_bytes(L.As, kStashC + kNodeBytes);
+    L.smem_p = pipe_smem_bytes(L.Ap, ex_p);
+    L.smem_t = pipe_smem_bytes(L.At, ex_t);
+    L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
     L.nb = (unsigned)B.nblocks;
     L.pg = pipe_grid(A);
+    L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
     int64_t ewg = (n + 255) / 256;
     int64_t cap = (int64_t)num_sms() * 8;
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
@@ -753,7 +825,7 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
             ZK_CUDA(cudaGetLastError());
             ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
             ZK_CUDA(cudaStreamSynchronize(s));
-            if (pe.on) accumulate(c, pe, 2, 8);
+            if (pe.on) accumulate(c, pe, 2, 9);
             if (out.done) break;
         }
         if (pe.on)

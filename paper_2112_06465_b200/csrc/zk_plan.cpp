@@ -88,6 +88,11 @@ size_t build_plan(int32_t L, int32_t kind, void* out) {
     h.nnodes = nleaves + ninner;
     h.root = (L > 0) ? node_id(root) : 0;
     h.nops = cnt;
+    for (int j = 0; j <= 129; ++j) {
+        int k = 0;  // leaves are in ascending position order
+        while (k < nleaves && 1 + B.leaf_start[k] + B.leaf_len[k] <= 32 * j) ++k;
+        h.leaf_upto[j] = (int16_t)k;
+    }
     size_t leaves_bytes = sizeof(int32_t) * 2 * (size_t)nleaves;
     size_t ops_bytes = sizeof(int32_t) * 4 * (size_t)cnt;
     h.leaves_off = (int32_t)((sizeof(PlanHeader) + 15) / 16 * 16);

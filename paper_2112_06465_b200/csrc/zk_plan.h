@@ -34,6 +34,10 @@ struct PlanHeader {
     int32_t ops_off;        // int4 (dst, a, b, 0) array, byte offset from header
     int32_t nops;
     int32_t pad;
+    // leaf_upto[j]: number of leaves whose elements all lie in rows [0, 32*j)
+    // of the 4096-row block (element e of the segment is block row 1+e); lets
+    // the SpMV kernels reduce leaves as soon as the rows under them are done.
+    int16_t leaf_upto[130];
 };
 
 // Builds the plan for segment length L into `out` (host memory); returns the

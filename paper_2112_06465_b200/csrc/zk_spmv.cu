@@ -1,5 +1,6 @@
 // zk_spmv.cu -- CSR -> SELL-32 conversion and the plain SpMV kernel.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -25,14 +26,39 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
     v.long_ia = A->long_ia;
     v.long_ja = A->long_ja;
     v.long_aa = A->long_aa;
+    // Ring chunk = (1 + 4 cm) columns of a slice (two pairwise groups, or one
+    // when shared memory is tight), independent of the row width.
+    v.win = A->n_long ? kBlock / kSlice : kWindowSlices;
     const int w = A->wmax > 0 ? A->wmax : 1;
-    v.ja_off = 32 * w * 16;
-    v.stage_bytes = (32 * w * 20 + 127) / 128 * 128;
     const long avail = (long)kSmemLimit - 1024 - kBarBytes - (long)extra;
-    int ns = (int)(avail / v.stage_bytes);
-    ns = ns > kMaxStages ? kMaxStages : (ns < 1 ? 1 : ns);
-    v.cw = ns < kConsumerWarps ? ns : kConsumerWarps;
-    v.ns = ns / v.cw * v.cw;
+    const char* env_cm = std::getenv("ZK_CM");      // tuning overrides (experiments only)
+    const char* env_ns = std::getenv("ZK_NS");
+    const int cm_hi = env_cm ? std::atoi(env_cm) : 2;
+    const int cm_lo = env_cm ? cm_hi : 1;
+    if ((!env_cm || cm_hi == 0) && w <= kFullCols) {  // whole slice per stage, whole-row prefetch
+        v.cm = 0;
+        v.nch = 1;
+        v.ja_off = w * kSlice * 16;
+        v.stage_bytes = (w * kSlice * 20 + 127) / 128 * 128;
+        const long ns = avail / v.stage_bytes;
+        const long cap = std::max<long>(10, 180 * 1024 / v.stage_bytes);  // deeper rings measured slower on C4
+        v.ns = (int)(ns > std::min<long>(cap, kMaxStages) ? std::min<long>(cap, kMaxStages) : (ns < 1 ? 1 : ns));
+        if (env_ns && std::atoi(env_ns) > 0 && std::atoi(env_ns) < v.ns) v.ns = std::atoi(env_ns);
+        v.swap = (A->nnz * 16 >= c->elide_bytes);
+        v.fma = c->fma != 0;
+        return v;
+    }
+    for (int cm = cm_hi; cm >= cm_lo; --cm) {
+        const int cols = 1 + 4 * cm;
+        v.cm = cm;
+        v.nch = w <= cols ? 1 : 1 + (w - cols + 4 * cm - 1) / (4 * cm);
+        v.ja_off = cols * kSlice * 16;
+        v.stage_bytes = (cols * kSlice * 20 + 127) / 128 * 128;
+        const long ns = avail / v.stage_bytes;
+        v.ns = (int)(ns > kMaxStages ? kMaxStages : (ns < 1 ? 1 : ns));
+        if (v.ns >= 20) break;
+    }
+    if (env_ns && std::atoi(env_ns) > 0 && std::atoi(env_ns) < v.ns) v.ns = std::atoi(env_ns);
     v.swap = (A->nnz * 16 >= c->elide_bytes);
     v.fma = c->fma != 0;
     return v;
@@ -92,7 +118,10 @@ __global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __
 
 struct PlainSpmv {
     double2* __restrict__ y;
-    __device__ __forceinline__ void row(int64_t r, double2 v) { y[r] = v; }
+    struct RowCtx {};
+    __device__ __forceinline__ RowCtx prefetch(int64_t) { return {}; }
+    __device__ __forceinline__ void row(int64_t r, double2 v, const RowCtx&) { y[r] = v; }
+    __device__ __forceinline__ void window_done(int64_t, int) {}
     __device__ __forceinline__ void block_done(int64_t) {}
 };
 

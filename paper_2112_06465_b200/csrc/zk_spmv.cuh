@@ -34,12 +34,18 @@
 
 namespace zk {
 
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 7;  // + 1 producer = 8 warps: 2 per SMSP, so up to 255 registers/thread
 constexpr int kConsumers = kConsumerWarps * 32;  // 256
 constexpr int kPipeThreads = kConsumers + 32;    // + producer warp
 constexpr int kMaxStages = 32;
-constexpr int kBarBytes = 2 * kMaxStages * 8;
+constexpr int kBarBytes = 2 * kMaxStages * 8 + kMaxStages * 4;  // full, empty mbarriers + stage tags
 constexpr int kSmemLimit = 227 * 1024;
+constexpr int kFullCols = 33;  // widest row handled by the whole-row prefetch path
+// Reduction windows: 28 slices (4 per consumer warp, 896 rows).  With a
+// 2048-row stash ring a window never overwrites rows a pending leaf (<= 128
+// elements) or the previous window's leaf pass still reads (896*2+128 < 2048).
+constexpr int kWindowSlices = 4 * kConsumerWarps;
+constexpr int kStashRows = 2048;
 
 struct SellView {
     int64_t n_rows, n_cols, nslices, nblocks;
@@ -52,10 +58,12 @@ struct SellView {
     const int64_t* __restrict__ long_ia;
     const int32_t* __restrict__ long_ja;
     const double2* __restrict__ long_aa;
-    int32_t stage_bytes;  // ring stage size (widest slice of the matrix, 128 B rounded)
+    int32_t cm;           // pairwise groups (4 columns each) per ring chunk; 0 = whole slice per stage
+    int32_t nch;          // chunks per slice (from the widest slice)
+    int32_t stage_bytes;  // (1 + 4 cm) columns x 32 rows x 20 B, 128 B rounded
     int32_t ja_off;       // byte offset of the column indices inside a stage
-    int32_t ns;           // ring stages for this launch (a multiple of cw)
-    int32_t cw;           // consumer warps that take slices (stage st is only ever read by warp st % cw)
+    int32_t ns;           // ring stages for this launch
+    int32_t win;          // slices per reduction window (kWindowSlices, or a whole block with long rows)
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
 };
@@ -64,45 +72,134 @@ __device__ __forceinline__ double2 spmv_prod(const SellView& A, double2 a, doubl
     return A.swap ? f1(xv, a, A.fma) : f1(a, xv, A.fma);
 }
 
-// Row sum of a short row from a ring stage (element k at [32*k + lane]).
-__device__ __forceinline__ double2 stage_row(const SellView& A, const double2* __restrict__ x,
-                                             const double2* saa, const int32_t* sja, int lane, int len) {
-    if (len == 0) return make_double2(0.0, 0.0);
-    double2 v0 = spmv_prod(A, saa[lane], __ldg(x + sja[lane]));
-    const int L = len - 1;
-    if (L == 0) return v0;
-    double2 s;
-    if (L < 4) {
+// Per-row accumulator of numpy's order, fed chunk by chunk (chunk c holds
+// columns [c0, c1) of the slice; chunk boundaries sit on pairwise-group
+// boundaries, so a group of four never straddles two chunks).
+struct RowAcc {
+    double2 v0, r0, r1, r2, r3, s;
+    int L, G;
+    bool combined;
+
+    __device__ __forceinline__ void init(int len) {
+        L = len - 1;
+        G = L >= 4 ? (L >> 2) : 0;
+        combined = false;
         s = make_double2(-0.0, -0.0);
-        for (int k = 1; k <= L; ++k) s = cadd(s, spmv_prod(A, saa[32 * k + lane], __ldg(x + sja[32 * k + lane])));
+    }
+
+    // saa/sja: the chunk's stage; element (k - c0) of this lane's row at [32*(k-c0) + lane]
+    __device__ __forceinline__ void chunk(const SellView& A, const double2* __restrict__ x, const double2* saa,
+                                          const int32_t* sja, int lane, int c, int c0) {
+        const int len = L + 1;
+        if (len <= 0) return;
+        auto prod = [&](int k) {
+            const int e = 32 * (k - c0) + lane;
+            return spmv_prod(A, saa[e], __ldg(x + sja[e]));
+        };
+        if (c == 0) v0 = prod(0);
+        if (L < 4) {  // sequential from -0.0 (2L < 8); len <= 4 <= 1+4cm: all in chunk 0
+            if (c == 0)
+                for (int k = 1; k <= L; ++k) s = cadd(s, prod(k));
+            return;
+        }
+        const int g_lo = (c == 0) ? 0 : A.cm * c;
+        const int g_hi = A.cm * (c + 1);
+        int g = g_lo;
+        if (g < G) {
+            double2 cx[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cx[q] = __ldg(x + sja[32 * (1 + 4 * g + q - c0) + lane]);
+            for (; g < g_hi && g < G; ++g) {
+                double2 nx[4];
+                const bool more = (g + 1 < g_hi) && (g + 1 < G);
+                if (more) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) nx[q] = __ldg(x + sja[32 * (5 + 4 * g + q - c0) + lane]);
+                }
+                const int kb = 32 * (1 + 4 * g - c0) + lane;
+                const double2 p0 = spmv_prod(A, saa[kb], cx[0]);
+                const double2 p1 = spmv_prod(A, saa[kb + 32], cx[1]);
+                const double2 p2 = spmv_prod(A, saa[kb + 64], cx[2]);
+                const double2 p3 = spmv_prod(A, saa[kb + 96], cx[3]);
+                if (g == 0) {
+                    r0 = p0; r1 = p1; r2 = p2; r3 = p3;
+                } else {
+                    r0 = cadd(r0, p0); r1 = cadd(r1, p1); r2 = cadd(r2, p2); r3 = cadd(r3, p3);
+                }
+                if (more) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) cx[q] = nx[q];
+                }
+            }
+        }
+        if (G >= g_lo && G < g_hi) {  // this chunk holds the end of the full groups: combine, add leftovers
+            s = cadd(cadd(r0, r1), cadd(r2, r3));
+            combined = true;
+            for (int k = 1 + 4 * G; k <= L; ++k) s = cadd(s, prod(k));
+        }
+    }
+
+    // Whole row in one chunk (width <= kFullCols).  The row's x gathers are
+    // issued in two batches (v0 + groups 0..3, then groups 4..7 and the
+    // leftovers), each batch fully in flight before its first product: two
+    // L1/L2 round trips per row instead of one per group.
+    __device__ __forceinline__ void full_row(const SellView& A, const double2* __restrict__ x, const double2* saa,
+                                             const int32_t* sja, int lane) {
+        const int len = L + 1;
+        if (len <= 0) return;
+        double2 xs[17];
+#pragma unroll
+        for (int k = 0; k < 17; ++k)
+            if (k < len) xs[k] = __ldg(x + sja[32 * k + lane]);
+        v0 = spmv_prod(A, saa[lane], xs[0]);
+        if (L < 4) {
+#pragma unroll
+            for (int k = 1; k < 4; ++k)
+                if (k <= L) s = cadd(s, spmv_prod(A, saa[32 * k + lane], xs[k]));
+            return;
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const int kb = 1 + 16 * half;  // first column of this batch
+            if (half == 1) {
+                if (L < 17) break;
+#pragma unroll
+                for (int t = 0; t < 16; ++t)
+                    if (kb + t <= L) xs[1 + t] = __ldg(x + sja[32 * (kb + t) + lane]);
+            }
+            // batch columns kb .. kb+15 live in xs[1 .. 16]
+#pragma unroll
+            for (int gg = 0; gg < 4; ++gg) {
+                const int g = 4 * half + gg;
+                if (g < G) {
+                    const double2 p0 = spmv_prod(A, saa[32 * (kb + 4 * gg) + lane], xs[1 + 4 * gg]);
+                    const double2 p1 = spmv_prod(A, saa[32 * (kb + 4 * gg + 1) + lane], xs[2 + 4 * gg]);
+                    const double2 p2 = spmv_prod(A, saa[32 * (kb + 4 * gg + 2) + lane], xs[3 + 4 * gg]);
+                    const double2 p3 = spmv_prod(A, saa[32 * (kb + 4 * gg + 3) + lane], xs[4 + 4 * gg]);
+                    if (g == 0) {
+                        r0 = p0; r1 = p1; r2 = p2; r3 = p3;
+                    } else {
+                        r0 = cadd(r0, p0); r1 = cadd(r1, p1); r2 = cadd(r2, p2); r3 = cadd(r3, p3);
+                    }
+                } else if (g == G) {  // full groups done: combine, then the (< 4) leftovers
+                    s = cadd(cadd(r0, r1), cadd(r2, r3));
+                    combined = true;
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        if (4 * gg + j < 16 && kb + 4 * gg + j <= L)
+                            s = cadd(s, spmv_prod(A, saa[32 * (kb + 4 * gg + j) + lane], xs[1 + 4 * gg + j]));
+                }
+            }
+        }
+    }
+
+    __device__ __forceinline__ double2 result() {
+        if (L < 0) return make_double2(0.0, 0.0);
+        if (L == 0) return v0;
+        if (L >= 4 && !combined) s = cadd(cadd(r0, r1), cadd(r2, r3));
         return cadd(v0, s);
     }
-    const int G = L >> 2;
-    double2 cx[4], r[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) cx[q] = __ldg(x + sja[32 * (1 + q) + lane]);
-    for (int g = 0; g < G; ++g) {
-        double2 nx[4];
-        const int kn = 1 + 4 * (g + 1);
-        if (g + 1 < G) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) nx[q] = __ldg(x + sja[32 * (kn + q) + lane]);
-        }
-        const int kc = 1 + 4 * g;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            double2 p = spmv_prod(A, saa[32 * (kc + q) + lane], cx[q]);
-            r[q] = (g == 0) ? p : cadd(r[q], p);
-        }
-        if (g + 1 < G) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) cx[q] = nx[q];
-        }
-    }
-    s = cadd(cadd(r[0], r[1]), cadd(r[2], r[3]));
-    for (int k = 1 + 4 * G; k <= L; ++k) s = cadd(s, spmv_prod(A, saa[32 * k + lane], __ldg(x + sja[32 * k + lane])));
-    return cadd(v0, s);
-}
+};
 
 __device__ __forceinline__ double2 long_prod(const SellView& A, const double2* __restrict__ x, int64_t idx) {
     return spmv_prod(A, A.long_aa[idx], __ldg(x + A.long_ja[idx]));
@@ -142,83 +239,133 @@ __device__ __forceinline__ double2 long_row_sum(const SellView& A, const double2
 }
 
 // Persistent pipelined SpMV over the CTA's 4096-row blocks (blk = blockIdx.x,
-// +gridDim.x, ...).  body.row(row, value) is called once per row by the
-// consumer thread that computed it; body.block_done(blk) is called by all
-// consumer threads after every row of the block is done (named barrier 1
-// already passed).  The producer warp exits when it has issued every slice.
-// `smem` points at kBarBytes + ns*stage_bytes bytes of dynamic shared memory.
+// +gridDim.x, ...).  For each row the consumer thread calls
+// ctx = body.prefetch(row) before the row's matrix chunks arrive (so the
+// epilogue operands are in flight during the row computation), then
+// body.row(row, value, ctx).  After every row of a block is done (named
+// barrier 1 passed) all consumer threads call body.block_done(blk).  The
+// producer warp exits once it has issued every chunk.  `smem` holds
+// kBarBytes + ns*stage_bytes bytes.
 template <class Body>
 __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* __restrict__ x, Body& body,
                                               unsigned char* smem) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
+    // tag[st] = CTA-local index of the chunk the producer last armed stage st
+    // for.  A consumer waits for its own tag before the parity wait on
+    // full[st]: the parity wait cannot tell use u from use u+2, and a
+    // consumer warp can reach use u+1 of a stage before use u has landed.
+    volatile uint32_t* tag = reinterpret_cast<volatile uint32_t*>(empty + kMaxStages);
     unsigned char* ring = smem + kBarBytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ns = A.ns;
+    const int ns = A.ns, nch = A.nch;
+    const int cols = 1 + 4 * A.cm;
     constexpr int kSlicesPerBlock = kBlock / kSlice;
     if (threadIdx.x == 0) {
         for (int i = 0; i < ns; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], 1);
+            tag[i] = 0xffffffffu;
         }
         mbar_fence_init();
     }
     __syncthreads();
-    if (warp == kConsumerWarps) {  // producer
-        if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
-            int64_t i = 0;
-            for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
-                const int64_t s_lo = blk * kSlicesPerBlock;
-                const int64_t s_hi = (s_lo + kSlicesPerBlock < A.nslices) ? s_lo + kSlicesPerBlock : A.nslices;
-                for (int64_t s = s_lo; s < s_hi; ++s, ++i) {
-                    const int st = (int)(i % ns);
-                    const int64_t u = i / ns;
-                    if (u) mbar_wait(&empty[st], (uint32_t)((u - 1) & 1));
-                    const int64_t off0 = __ldg(A.slice_off + s);
-                    const uint32_t cnt = (uint32_t)(__ldg(A.slice_off + s + 1) - off0);
-                    mbar_arrive_expect_tx(&full[st], cnt * 20u);
-                    if (cnt) {
-                        unsigned char* stage = ring + (size_t)st * A.stage_bytes;
-                        bulk_g2s(stage, A.aa + off0, cnt * 16u, &full[st], pol);
-                        bulk_g2s(stage + A.ja_off, A.ja + off0, cnt * 4u, &full[st], pol);
-                    }
+    if (warp == kConsumerWarps) {  // producer warp: lane l owns ring stage l
+        // Chunk i of the CTA's sequence uses stage i % ns, so lane l issues
+        // chunks l, l + ns, l + 2ns, ... in order; each lane polls its own
+        // empty barrier without blocking, so the lanes progress independently
+        // and one warp instruction issues up to 32 bulk copies.
+        const uint64_t pol = l2_evict_first_policy();
+        const bool owner = lane < ns;
+        uint32_t i = (uint32_t)lane, u = 0;
+        int64_t off0 = 0, off1 = 0;
+        int c = 0, w = 0;
+        bool active = false;
+        auto locate = [&]() {  // coordinates + offsets of chunk i (loads issued early)
+            const uint32_t seq = i / (uint32_t)nch;
+            c = (int)(i % (uint32_t)nch);
+            const int64_t blk = blockIdx.x + (int64_t)(seq / kSlicesPerBlock) * gridDim.x;
+            const int64_t s = blk * kSlicesPerBlock + (seq % kSlicesPerBlock);
+            active = blk < A.nblocks && s < A.nslices;
+            if (active) {
+                off0 = __ldg(A.slice_off + s);
+                off1 = __ldg(A.slice_off + s + 1);
+            }
+        };
+        if (owner) locate();
+        while (__any_sync(0xffffffffu, owner && active)) {
+            if (owner && active && (u == 0 || mbar_test(&empty[lane], (u - 1) & 1))) {
+                w = (int)((off1 - off0) / kSlice);
+                tag[lane] = i;
+                const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
+                const int c1 = A.cm == 0 ? w : min(w, cols + 4 * A.cm * c);
+                const uint32_t cnt = c1 > c0 ? (uint32_t)(c1 - c0) * kSlice : 0u;
+                mbar_arrive_expect_tx(&full[lane], cnt * 20u);
+                if (cnt) {
+                    unsigned char* stage = ring + (size_t)lane * A.stage_bytes;
+                    const int64_t off = off0 + (int64_t)c0 * kSlice;
+                    bulk_g2s(stage, A.aa + off, cnt * 16u, &full[lane], pol);
+                    bulk_g2s(stage + A.ja_off, A.ja + off, cnt * 4u, &full[lane], pol);
                 }
+                i += (uint32_t)ns;
+                ++u;
+                locate();
             }
         }
         return;
     }
-    // Slice i of the CTA's sequence goes to stage i % ns and to warp i % cw.
-    // Because ns is a multiple of cw, every stage has exactly one consumer
-    // warp and that warp meets the stage's uses in order -- required by the
-    // parity wait, which cannot tell use u from use u+2.
-    const int cw = A.cw;
-    int64_t ibase = 0;
+    uint32_t sbase = 0;  // CTA-local index of the block's first slice
     for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
         const int64_t s_lo = blk * kSlicesPerBlock;
         const int64_t s_hi = (s_lo + kSlicesPerBlock < A.nslices) ? s_lo + kSlicesPerBlock : A.nslices;
         const int nsl = (int)(s_hi - s_lo);
-        const int j0 = warp < cw ? (int)(((int64_t)warp - ibase % cw + cw) % cw) : nsl;
-        for (int j = j0; j < nsl; j += cw) {
-            const int64_t i = ibase + j;
-            const int st = (int)(i % ns);
+        // windows of A.win slices; after each (but the last) the body may
+        // reduce everything that lies entirely in the rows done so far
+        for (int w0 = 0; w0 < nsl; w0 += A.win) {
+        const int w1 = min(nsl, w0 + A.win);
+        for (int j = w0 + warp; j < w1; j += kConsumerWarps) {
             const int64_t row = (s_lo + j) * kSlice + lane;
             const int len = A.rowlen[row];
-            mbar_wait(&full[st], (uint32_t)((i / ns) & 1));
-            const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
-            if (row < A.n_rows && len != 255) {
-                double2 v = stage_row(A, x, reinterpret_cast<const double2*>(stage),
-                                      reinterpret_cast<const int32_t*>(stage + A.ja_off), lane, len);
-                body.row(row, v);
+            const bool mine = row < A.n_rows && len != 255;
+            typename Body::RowCtx ctx;
+            if (mine) ctx = body.prefetch(row);
+            RowAcc acc;
+            acc.init(mine ? len : 0);
+            for (int c = 0; c < nch; ++c) {
+                const uint32_t i = (sbase + (uint32_t)j) * (uint32_t)nch + (uint32_t)c;
+                const int st = (int)(i % ns);
+                while (tag[st] != i) {
+                }
+                mbar_wait(&full[st], (i / ns) & 1);
+                const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
+                if (A.cm == 0) {
+                    if (mine)
+                        acc.full_row(A, x, reinterpret_cast<const double2*>(stage),
+                                     reinterpret_cast<const int32_t*>(stage + A.ja_off), lane);
+                } else {
+                    const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
+                    if (mine && len > c0)
+                        acc.chunk(A, x, reinterpret_cast<const double2*>(stage),
+                                  reinterpret_cast<const int32_t*>(stage + A.ja_off), lane, c, c0);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
+            if (mine) body.row(row, acc.result(), ctx);
         }
-        ibase += nsl;
+        if (w1 < nsl) {
+            named_sync(1, kConsumers);
+            body.window_done(blk, w1);
+        }
+        }
+        sbase += (uint32_t)nsl;
         if (A.long_blk_ptr) {
             const int lb = A.long_blk_ptr[blk], le = A.long_blk_ptr[blk + 1];
-            for (int li = lb + (int)threadIdx.x; li < le; li += kConsumers)
-                body.row((int64_t)A.long_row[li], long_row_sum(A, x, li));
+            for (int li = lb + (int)threadIdx.x; li < le; li += kConsumers) {
+                const int64_t row = (int64_t)A.long_row[li];
+                typename Body::RowCtx ctx = body.prefetch(row);
+                body.row(row, long_row_sum(A, x, li), ctx);
+            }
         }
         named_sync(1, kConsumers);
         body.block_done(blk);

@@ -1,0 +1,30 @@
+"""Standalone zSpMV timing on C4 for the ring-geometry sweep (env ZK_CM / ZK_NS)."""
+import json
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2112_06465_b200 as Z  # noqa: E402
+from paper_2112_06465_b200 import _lib, problems  # noqa: E402
+
+m = int(os.environ.get("ZK_PROFILE_M", "200"))
+n, ia, ja, aa, b = problems.helmholtz_27pt(m)
+A = Z.CsrMatrix(n, n, aa, ja, ia)
+x = Z.ZVector(np.random.default_rng(0).random(n) + 0j)
+res = {}
+for cm in ("0", "2"):
+    for ns in ("6", "8", "10", "12", "32"):
+        os.environ["ZK_CM"], os.environ["ZK_NS"] = cm, ns
+        Z.spmv(A, x)
+        _lib.synchronize()
+        _lib.event_record(0)
+        for _ in range(10):
+            Z.spmv(A, x)
+        _lib.event_record(1)
+        us = _lib.event_elapsed_ms(0, 1) / 10 * 1e3
+        res[f"cm{cm}_ns{ns}"] = round(us, 1)
+bytes_ = 20 * ia[-1] + 4 * (n + 1) + 32 * n
+best = min(res, key=res.get)
+print(json.dumps({"us": res, "best": best, "best_gbs": round(bytes_ / (res[best] * 1e-6) / 1e9, 1)}))
