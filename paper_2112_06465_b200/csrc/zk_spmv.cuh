@@ -151,6 +151,7 @@ struct RowAcc {
 #pragma unroll
         for (int k = 0; k < 17; ++k)
             if (k < len) xs[k] = __ldg(x + sja[32 * k + lane]);
+        asm volatile("" ::: "memory");  // keep the value loads below the gathers (register pressure)
         v0 = spmv_prod(A, saa[lane], xs[0]);
         if (L < 4) {
 #pragma unroll
@@ -166,6 +167,7 @@ struct RowAcc {
 #pragma unroll
                 for (int t = 0; t < 16; ++t)
                     if (kb + t <= L) xs[1 + t] = __ldg(x + sja[32 * (kb + t) + lane]);
+                asm volatile("" ::: "memory");
             }
             // batch columns kb .. kb+15 live in xs[1 .. 16]
 #pragma unroll
@@ -205,31 +207,57 @@ __device__ __forceinline__ double2 long_prod(const SellView& A, const double2* _
     return spmv_prod(A, A.long_aa[idx], __ldg(x + A.long_ja[idx]));
 }
 
-// numpy CDOUBLE_pairwise_sum over products [s, s+L) of the side CSR.
-static __device__ double2 long_pw(const SellView& A, const double2* __restrict__ x, int64_t s, int64_t L) {
-    if (L < 4) {
-        double2 acc = make_double2(-0.0, -0.0);
-        for (int64_t k = 0; k < L; ++k) acc = cadd(acc, long_prod(A, x, s + k));
-        return acc;
-    }
-    if (L <= 64) {
-        double2 r0 = long_prod(A, x, s), r1 = long_prod(A, x, s + 1);
-        double2 r2 = long_prod(A, x, s + 2), r3 = long_prod(A, x, s + 3);
-        const int64_t G = L / 4;
-        for (int64_t g = 1; g < G; ++g) {
-            r0 = cadd(r0, long_prod(A, x, s + 4 * g));
-            r1 = cadd(r1, long_prod(A, x, s + 4 * g + 1));
-            r2 = cadd(r2, long_prod(A, x, s + 4 * g + 2));
-            r3 = cadd(r3, long_prod(A, x, s + 4 * g + 3));
+// numpy CDOUBLE_pairwise_sum over products [s, s+L) of the side CSR,
+// evaluated iteratively (explicit post-order stack; no device recursion, so
+// the calling kernels keep their register allocation).
+static __device__ __noinline__ double2 long_pw(const SellView& A, const double2* __restrict__ x, int64_t s, int64_t L) {
+    int64_t fs[40], fl[40];
+    int8_t fphase[40];
+    double2 vals[40];
+    int sp = 0, vp = 0;
+    fs[0] = s;
+    fl[0] = L;
+    fphase[0] = 0;
+    sp = 1;
+    while (sp > 0) {
+        const int64_t cs = fs[sp - 1], cl = fl[sp - 1];
+        if (cl <= 64) {  // leaf
+            double2 acc;
+            if (cl < 4) {
+                acc = make_double2(-0.0, -0.0);
+                for (int64_t k = 0; k < cl; ++k) acc = cadd(acc, long_prod(A, x, cs + k));
+            } else {
+                double2 r0 = long_prod(A, x, cs), r1 = long_prod(A, x, cs + 1);
+                double2 r2 = long_prod(A, x, cs + 2), r3 = long_prod(A, x, cs + 3);
+                const int64_t G = cl / 4;
+                for (int64_t g = 1; g < G; ++g) {
+                    r0 = cadd(r0, long_prod(A, x, cs + 4 * g));
+                    r1 = cadd(r1, long_prod(A, x, cs + 4 * g + 1));
+                    r2 = cadd(r2, long_prod(A, x, cs + 4 * g + 2));
+                    r3 = cadd(r3, long_prod(A, x, cs + 4 * g + 3));
+                }
+                acc = cadd(cadd(r0, r1), cadd(r2, r3));
+                for (int64_t k = 4 * G; k < cl; ++k) acc = cadd(acc, long_prod(A, x, cs + k));
+            }
+            vals[vp++] = acc;
+            --sp;
+            continue;
         }
-        double2 acc = cadd(cadd(r0, r1), cadd(r2, r3));
-        for (int64_t k = 4 * G; k < L; ++k) acc = cadd(acc, long_prod(A, x, s + k));
-        return acc;
+        const int64_t h = (cl - cl % 8) / 2;
+        if (fphase[sp - 1] == 0) {  // descend left
+            fphase[sp - 1] = 1;
+            fs[sp] = cs; fl[sp] = h; fphase[sp] = 0; ++sp;
+        } else if (fphase[sp - 1] == 1) {  // descend right
+            fphase[sp - 1] = 2;
+            fs[sp] = cs + h; fl[sp] = cl - h; fphase[sp] = 0; ++sp;
+        } else {  // both halves done: combine left + right
+            const double2 b = vals[--vp];
+            const double2 a = vals[--vp];
+            vals[vp++] = cadd(a, b);
+            --sp;
+        }
     }
-    const int64_t h = (L - L % 8) / 2;
-    double2 a = long_pw(A, x, s, h);
-    double2 b = long_pw(A, x, s + h, L - h);
-    return cadd(a, b);
+    return vals[0];
 }
 
 __device__ __forceinline__ double2 long_row_sum(const SellView& A, const double2* __restrict__ x, int li) {
