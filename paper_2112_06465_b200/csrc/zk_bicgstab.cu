@@ -195,6 +195,7 @@ struct WinRed {
 // ---- setup: r0 = b - A x0, ||b||, ||r0||, <r0, r0> (krylov.py:159-168, 255) ----
 // Runs once per solve; uses the plain (CTA-wide) block reduction.
 struct SetupBody {
+    static constexpr bool kReduce = true;
     SolverBufs B;
     PlanPtrs pc, pr;
     double2* stash;
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_setup(SellView A, SolverBuf
     unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
     SetupBody body{B, pc, pr, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag,
                    s_res};
-    sell_pipeline(A, B.x, body, smem);
+    sell_run(A, B.x, body, smem);
 }
 
 __device__ __forceinline__ int stash_rows(const SellView& A) { return A.win < kBlock / kSlice ? kStashRows : kBlock; }
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(256) k_p_next(SolverBufs B) {
 
 // ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
 struct PivotBody {
+    static constexpr bool kReduce = true;
     SolverBufs B;
     WinRed<double2, 1> red;
     struct RowCtx { double2 rs; };
@@ -342,11 +344,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_pivot(SellView A, Solv
     const int rows = stash_rows(A);
     PivotBody body{B, {pc.full, pc.tail, reinterpret_cast<double2*>(extra), rows - 1,
                        reinterpret_cast<double2*>(extra + rows * sizeof(double2)), 0, 0, false, {}}};
-    sell_pipeline(A, B.ph, body, smem);
+    sell_run(A, B.ph, body, smem);
 }
 
 // ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
 struct TBody {
+    static constexpr bool kReduce = true;
     SolverBufs B;
     WinRed<double2, 2> red;
     struct RowCtx { double2 s; };
@@ -383,13 +386,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_t(SellView A, SolverBu
     const int rows = stash_rows(A);
     TBody body{B, {pc.full, pc.tail, reinterpret_cast<double2*>(extra), rows - 1,
                    reinterpret_cast<double2*>(extra + 2 * rows * sizeof(double2)), 0, 0, false, {}}};
-    sell_pipeline(A, B.sh, body, smem);
+    sell_run(A, B.sh, body, smem);
 }
 
 // ---- true residual ||b + F1(-1, A x)|| / ||b|| (krylov.py:183-186) ----
 // MODE 0: on the s-check path (K6x);  MODE 1: end of iteration (K61).
 template <int MODE>
 struct ResBody {
+    static constexpr bool kReduce = true;
     SolverBufs B;
     WinRed<double, 1> red;
     cudaGraphConditionalHandle cond;
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_true_res(SellView A, Solver
     ResBody<MODE> body{B, {pr.full, pr.tail, reinterpret_cast<double*>(extra), rows - 1,
                            reinterpret_cast<double*>(extra + rows * sizeof(double)), 0, 0, false, {}},
                        cond, use_cond};
-    sell_pipeline(A, B.x, body, smem);
+    sell_run(A, B.x, body, smem);
 }
 
 // ---- persistent block-pass kernels for the fused level-1 phases ----------

@@ -36,16 +36,21 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
     const int cm_hi = env_cm ? std::atoi(env_cm) : 2;
     const int cm_lo = env_cm ? cm_hi : 1;
     if ((!env_cm || cm_hi == 0) && w <= kFullCols) {  // whole slice per stage, whole-row prefetch
+        // stage = [aa: wpad x 32 double2][ja: wpad x 32 int32][32 row lengths],
+        // wpad = w rounded up to 4 (the fast row path reads whole groups)
+        const int wpad = (w + 3) & ~3;
         v.cm = 0;
         v.nch = 1;
-        v.ja_off = w * kSlice * 16;
-        v.stage_bytes = (w * kSlice * 20 + 127) / 128 * 128;
+        v.ja_off = wpad * kSlice * 16;
+        v.rl_off = v.ja_off + wpad * kSlice * 4;
+        v.stage_bytes = (v.rl_off + kSlice + 127) / 128 * 128;
         const long ns = avail / v.stage_bytes;
         const long cap = std::max<long>(10, 180 * 1024 / v.stage_bytes);  // deeper rings measured slower on C4
         v.ns = (int)(ns > std::min<long>(cap, kMaxStages) ? std::min<long>(cap, kMaxStages) : (ns < 1 ? 1 : ns));
         if (env_ns && std::atoi(env_ns) > 0 && std::atoi(env_ns) < v.ns) v.ns = std::atoi(env_ns);
         v.swap = (A->nnz * 16 >= c->elide_bytes);
         v.fma = c->fma != 0;
+        v.ns_magic = (uint32_t)((1ull << 32) / (uint64_t)v.ns + 1);
         return v;
     }
     for (int cm = cm_hi; cm >= cm_lo; --cm) {
@@ -53,6 +58,7 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
         v.cm = cm;
         v.nch = w <= cols ? 1 : 1 + (w - cols + 4 * cm - 1) / (4 * cm);
         v.ja_off = cols * kSlice * 16;
+        v.rl_off = 0;
         v.stage_bytes = (cols * kSlice * 20 + 127) / 128 * 128;
         const long ns = avail / v.stage_bytes;
         v.ns = (int)(ns > kMaxStages ? kMaxStages : (ns < 1 ? 1 : ns));
@@ -61,6 +67,7 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
     if (env_ns && std::atoi(env_ns) > 0 && std::atoi(env_ns) < v.ns) v.ns = std::atoi(env_ns);
     v.swap = (A->nnz * 16 >= c->elide_bytes);
     v.fma = c->fma != 0;
+    v.ns_magic = (uint32_t)((1ull << 32) / (uint64_t)v.ns + 1);
     return v;
 }
 
@@ -117,6 +124,7 @@ __global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __
 }
 
 struct PlainSpmv {
+    static constexpr bool kReduce = false;
     double2* __restrict__ y;
     struct RowCtx {};
     __device__ __forceinline__ RowCtx prefetch(int64_t) { return {}; }
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv(SellView A, const doub
                                                           double2* __restrict__ y) {
     extern __shared__ __align__(128) unsigned char smem[];
     PlainSpmv body{y};
-    sell_pipeline(A, x, body, smem);
+    sell_run(A, x, body, smem);
 }
 
 template <class T>

@@ -38,7 +38,7 @@ constexpr int kConsumerWarps = 7;  // + 1 producer = 8 warps: 2 per SMSP, so up 
 constexpr int kConsumers = kConsumerWarps * 32;  // 256
 constexpr int kPipeThreads = kConsumers + 32;    // + producer warp
 constexpr int kMaxStages = 32;
-constexpr int kBarBytes = 2 * kMaxStages * 8 + kMaxStages * 4;  // full, empty mbarriers + stage tags
+constexpr int kBarBytes = 2 * kMaxStages * 8 + 2 * kMaxStages * 4;  // full, empty mbarriers + stage tags, widths
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kFullCols = 33;  // widest row handled by the whole-row prefetch path
 // Reduction windows: 28 slices (4 per consumer warp, 896 rows).  With a
@@ -62,7 +62,9 @@ struct SellView {
     int32_t nch;          // chunks per slice (from the widest slice)
     int32_t stage_bytes;  // (1 + 4 cm) columns x 32 rows x 20 B, 128 B rounded
     int32_t ja_off;       // byte offset of the column indices inside a stage
+    int32_t rl_off;       // byte offset of the slice's 32 row lengths inside a stage (cm == 0)
     int32_t ns;           // ring stages for this launch
+    uint32_t ns_magic;    // floor(2^32 / ns) + 1: i / ns = umulhi(i, ns_magic) for i < 2^27
     int32_t win;          // slices per reduction window (kWindowSlices, or a whole block with long rows)
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
@@ -266,15 +268,93 @@ __device__ __forceinline__ double2 long_row_sum(const SellView& A, const double2
     return cadd(v0, long_pw(A, x, lo + 1, L - 1));
 }
 
+// ---- fast row path (whole slice per stage, FMA fingerprint) --------------
+// One thread, one row of length len <= W4 (W4 = the slice width rounded up to
+// 4, warp-uniform, a compile-time constant here).  All gathers of the row
+// are issued before the first product; the pairwise order is evaluated with
+// predication instead of branches: element k (>= 1) belongs to lane
+// accumulator q = (k-1)%4 while its group g = (k-1)/4 is below G = L/4,
+// else (g == G) it is leftover q, added after the (l0+l1)+(l2+l3) combine.
+template <bool SWAP>
+__device__ __forceinline__ double2 prod_fma(double2 a, double2 xv) {
+    return SWAP ? f1(xv, a, true) : f1(a, xv, true);
+}
+
+template <int W4, bool SWAP>
+__device__ __forceinline__ double2 row_fast(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                            int lane, int len) {
+    constexpr int B1 = W4 < 28 ? W4 : 28;  // gathers in flight per batch (register budget)
+    const double2 z = make_double2(0.0, 0.0);
+    const int L = len - 1;
+    const int G = L >> 2;
+    const int rem = L - 4 * G;
+    double2 r[4] = {z, z, z, z}, lo[3] = {z, z, z};
+    double2 v0 = z;
+    double2 xs[B1];
+#pragma unroll
+    for (int k = 0; k < B1; ++k) {
+        xs[k] = z;
+        if (k < len) xs[k] = __ldg(x + sja[32 * k + lane]);
+    }
+#pragma unroll
+    for (int k = 0; k < W4; ++k) {
+        if (k == B1) {  // second batch (rows wider than 28)
+#pragma unroll
+            for (int t = 0; t < W4 - B1; ++t) {
+                xs[t] = z;
+                if (B1 + t < len) xs[t] = __ldg(x + sja[32 * (B1 + t) + lane]);
+            }
+        }
+        const double2 p = prod_fma<SWAP>(saa[32 * k + lane], xs[k < B1 ? k : k - B1]);
+        if (k == 0) {
+            v0 = p;
+            continue;
+        }
+        const int g = (k - 1) >> 2, q = (k - 1) & 3;
+        if (g < G) {
+            r[q] = (g == 0) ? p : cadd(r[q], p);
+        } else if (q < 3 && g == G) {
+            lo[q] = p;
+        }
+    }
+    double2 s = make_double2(-0.0, -0.0);
+    if (G > 0) s = cadd(cadd(r[0], r[1]), cadd(r[2], r[3]));
+    if (rem > 0) s = cadd(s, lo[0]);
+    if (rem > 1) s = cadd(s, lo[1]);
+    if (rem > 2) s = cadd(s, lo[2]);
+    if (len <= 0) return z;
+    if (len == 1) return v0;
+    return cadd(v0, s);
+}
+
+template <bool SWAP>
+__device__ __forceinline__ double2 row_fast_dispatch(int W, const double2* __restrict__ x, const double2* saa,
+                                                     const int32_t* sja, int lane, int len) {
+    switch ((W + 3) >> 2) {
+        case 0:
+        case 1: return row_fast<4, SWAP>(x, saa, sja, lane, len);
+        case 2: return row_fast<8, SWAP>(x, saa, sja, lane, len);
+        case 3: return row_fast<12, SWAP>(x, saa, sja, lane, len);
+        case 4: return row_fast<16, SWAP>(x, saa, sja, lane, len);
+        case 5: return row_fast<20, SWAP>(x, saa, sja, lane, len);
+        case 6: return row_fast<24, SWAP>(x, saa, sja, lane, len);
+        case 7: return row_fast<28, SWAP>(x, saa, sja, lane, len);
+        case 8: return row_fast<32, SWAP>(x, saa, sja, lane, len);
+        default: return row_fast<36, SWAP>(x, saa, sja, lane, len);
+    }
+}
+
 // Persistent pipelined SpMV over the CTA's 4096-row blocks (blk = blockIdx.x,
 // +gridDim.x, ...).  For each row the consumer thread calls
-// ctx = body.prefetch(row) before the row's matrix chunks arrive (so the
-// epilogue operands are in flight during the row computation), then
-// body.row(row, value, ctx).  After every row of a block is done (named
-// barrier 1 passed) all consumer threads call body.block_done(blk).  The
-// producer warp exits once it has issued every chunk.  `smem` holds
+// ctx = body.prefetch(row) before the row's products (so the epilogue
+// operands are in flight during the row computation), then
+// body.row(row, value, ctx).  Bodies with reductions (Body::kReduce) get
+// window_done(blk, slices) after every window of A.win slices and
+// block_done(blk) after the block's last row, each behind a named barrier
+// over the consumer warps; plain bodies never synchronise the consumers.
+// The producer warp exits once it has issued every chunk.  `smem` holds
 // kBarBytes + ns*stage_bytes bytes.
-template <class Body>
+template <bool SWAP, class Body>
 __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* __restrict__ x, Body& body,
                                               unsigned char* smem) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -284,6 +364,9 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
     // full[st]: the parity wait cannot tell use u from use u+2, and a
     // consumer warp can reach use u+1 of a stage before use u has landed.
     volatile uint32_t* tag = reinterpret_cast<volatile uint32_t*>(empty + kMaxStages);
+    // wid[st] = width (entries per row) of the slice in stage st (cm == 0),
+    // written before the stage's arrive: visible after the full-barrier wait
+    uint32_t* wid = reinterpret_cast<uint32_t*>(empty + kMaxStages) + kMaxStages;
     unsigned char* ring = smem + kBarBytes;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ns = A.ns, nch = A.nch;
@@ -306,14 +389,14 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
         const uint64_t pol = l2_evict_first_policy();
         const bool owner = lane < ns;
         uint32_t i = (uint32_t)lane, u = 0;
-        int64_t off0 = 0, off1 = 0;
+        int64_t off0 = 0, off1 = 0, s = 0;
         int c = 0, w = 0;
         bool active = false;
         auto locate = [&]() {  // coordinates + offsets of chunk i (loads issued early)
             const uint32_t seq = i / (uint32_t)nch;
             c = (int)(i % (uint32_t)nch);
             const int64_t blk = blockIdx.x + (int64_t)(seq / kSlicesPerBlock) * gridDim.x;
-            const int64_t s = blk * kSlicesPerBlock + (seq % kSlicesPerBlock);
+            s = blk * kSlicesPerBlock + (seq % kSlicesPerBlock);
             active = blk < A.nblocks && s < A.nslices;
             if (active) {
                 off0 = __ldg(A.slice_off + s);
@@ -325,15 +408,26 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             if (owner && active && (u == 0 || mbar_test(&empty[lane], (u - 1) & 1))) {
                 w = (int)((off1 - off0) / kSlice);
                 tag[lane] = i;
-                const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
-                const int c1 = A.cm == 0 ? w : min(w, cols + 4 * A.cm * c);
-                const uint32_t cnt = c1 > c0 ? (uint32_t)(c1 - c0) * kSlice : 0u;
-                mbar_arrive_expect_tx(&full[lane], cnt * 20u);
-                if (cnt) {
-                    unsigned char* stage = ring + (size_t)lane * A.stage_bytes;
-                    const int64_t off = off0 + (int64_t)c0 * kSlice;
-                    bulk_g2s(stage, A.aa + off, cnt * 16u, &full[lane], pol);
-                    bulk_g2s(stage + A.ja_off, A.ja + off, cnt * 4u, &full[lane], pol);
+                unsigned char* stage = ring + (size_t)lane * A.stage_bytes;
+                if (A.cm == 0) {  // whole slice + its row lengths
+                    wid[lane] = (uint32_t)w;
+                    const uint32_t cnt = (uint32_t)w * kSlice;
+                    mbar_arrive_expect_tx(&full[lane], cnt * 20u + kSlice);
+                    if (cnt) {
+                        bulk_g2s(stage, A.aa + off0, cnt * 16u, &full[lane], pol);
+                        bulk_g2s(stage + A.ja_off, A.ja + off0, cnt * 4u, &full[lane], pol);
+                    }
+                    bulk_g2s(stage + A.rl_off, A.rowlen + s * kSlice, kSlice, &full[lane], pol);
+                } else {
+                    const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
+                    const int c1 = min(w, cols + 4 * A.cm * c);
+                    const uint32_t cnt = c1 > c0 ? (uint32_t)(c1 - c0) * kSlice : 0u;
+                    mbar_arrive_expect_tx(&full[lane], cnt * 20u);
+                    if (cnt) {
+                        const int64_t off = off0 + (int64_t)c0 * kSlice;
+                        bulk_g2s(stage, A.aa + off, cnt * 16u, &full[lane], pol);
+                        bulk_g2s(stage + A.ja_off, A.ja + off, cnt * 4u, &full[lane], pol);
+                    }
                 }
                 i += (uint32_t)ns;
                 ++u;
@@ -342,6 +436,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
         }
         return;
     }
+    const bool fast = A.cm == 0 && A.fma;
     uint32_t sbase = 0;  // CTA-local index of the block's first slice
     for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
         const int64_t s_lo = blk * kSlicesPerBlock;
@@ -349,10 +444,32 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
         const int nsl = (int)(s_hi - s_lo);
         // windows of A.win slices; after each (but the last) the body may
         // reduce everything that lies entirely in the rows done so far
-        for (int w0 = 0; w0 < nsl; w0 += A.win) {
-        const int w1 = min(nsl, w0 + A.win);
+        const int win = Body::kReduce ? A.win : nsl;
+        for (int w0 = 0; w0 < nsl; w0 += win) {
+        const int w1 = min(nsl, w0 + win);
         for (int j = w0 + warp; j < w1; j += kConsumerWarps) {
             const int64_t row = (s_lo + j) * kSlice + lane;
+            if (fast) {
+                const uint32_t i = sbase + (uint32_t)j;
+                const uint32_t q = __umulhi(i, A.ns_magic);
+                const int st = (int)(i - q * (uint32_t)ns);
+                while (tag[st] != i) {
+                }
+                mbar_wait(&full[st], q & 1);
+                const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
+                const int W = (int)wid[st];
+                const int len = stage[A.rl_off + lane];
+                const bool mine = row < A.n_rows && len != 255;
+                typename Body::RowCtx ctx;
+                if (mine) ctx = body.prefetch(row);
+                const double2 val = row_fast_dispatch<SWAP>(W, x, reinterpret_cast<const double2*>(stage),
+                                                            reinterpret_cast<const int32_t*>(stage + A.ja_off),
+                                                            lane, mine ? len : 0);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                if (mine) body.row(row, val, ctx);
+                continue;
+            }
             const int len = A.rowlen[row];
             const bool mine = row < A.n_rows && len != 255;
             typename Body::RowCtx ctx;
@@ -381,7 +498,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             }
             if (mine) body.row(row, acc.result(), ctx);
         }
-        if (w1 < nsl) {
+        if (Body::kReduce && w1 < nsl) {
             named_sync(1, kConsumers);
             body.window_done(blk, w1);
         }
@@ -395,9 +512,19 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
                 body.row(row, long_row_sum(A, x, li), ctx);
             }
         }
-        named_sync(1, kConsumers);
-        body.block_done(blk);
+        if (Body::kReduce) {
+            named_sync(1, kConsumers);
+            body.block_done(blk);
+        }
     }
+}
+
+// Kernel-side dispatch on numpy's elision swap (a launch-uniform flag).
+template <class Body>
+__device__ __forceinline__ void sell_run(const SellView& A, const double2* __restrict__ x, Body& body,
+                                         unsigned char* smem) {
+    if (A.swap) sell_pipeline<true>(A, x, body, smem);
+    else sell_pipeline<false>(A, x, body, smem);
 }
 
 }  // namespace zk
