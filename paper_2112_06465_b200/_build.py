@@ -20,13 +20,13 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-
          "-I" + os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 
 
-def _obj(src):
-    return os.path.join(OUT_DIR, "obj", os.path.splitext(src)[0] + ".o")
+def _obj(src, out_dir=OUT_DIR):
+    return os.path.join(out_dir, "obj", os.path.splitext(src)[0] + ".o")
 
 
-def _compile(src, verbose=False):
-    obj = _obj(src)
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+def _compile(src, verbose=False, out_dir=OUT_DIR, defines=()):
+    obj = _obj(src, out_dir)
+    cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
     if verbose and src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -46,24 +46,27 @@ def _stale():
     return False
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out_dir: str = OUT_DIR, defines=()) -> str:
+    """Build libzk.so into out_dir (default: the package's lib/).  A different
+    out_dir + defines builds a kernel variant for A/B experiments."""
+    out = os.path.join(out_dir, "libzk.so")
+    if out_dir == OUT_DIR and not defines and not force and not _stale():
         return OUT
-    os.makedirs(os.path.join(OUT_DIR, "obj"), exist_ok=True)
+    os.makedirs(os.path.join(out_dir, "obj"), exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        logs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
+        logs = list(ex.map(lambda s: _compile(s, verbose, out_dir, defines), SOURCES))
     if verbose:
         for s, l in zip(SOURCES, logs):
             if l.strip():
                 print(f"== {s}\n{l}", file=sys.stderr)
-    tmp = OUT + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[_obj(s) for s in SOURCES], "-lcudart_static", "-lrt", "-ldl",
+    tmp = out + ".tmp"
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[_obj(s, out_dir) for s in SOURCES], "-lcudart_static", "-lrt", "-ldl",
            "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

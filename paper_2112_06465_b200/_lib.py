@@ -114,7 +114,8 @@ def load_library():
             _build.build()
         except Exception as exc:  # noqa: BLE001
             raise DeviceUnavailableError(f"libzk.so is missing and could not be built: {exc}") from exc
-    lib = ctypes.CDLL(LIB_PATH)
+    # ZK_LIB_PATH: load an alternative build (kernel-variant experiments only)
+    lib = ctypes.CDLL(os.environ.get("ZK_LIB_PATH", LIB_PATH))
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -184,8 +185,8 @@ def launch_count() -> int:
     return c.value
 
 
-PHASES = ("setup", "p_first", "spmv_pivot", "s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update",
-          "p_next", "true_res")
+PHASES = ("setup", "p_first", "pivot_first", "s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update",
+          "true_res", "p_next", "spmv_pivot")
 
 
 def event_record(slot: int) -> None:

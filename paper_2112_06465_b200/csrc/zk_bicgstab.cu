@@ -32,7 +32,7 @@
 
 namespace zk {
 
-SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra);
+SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv);
 size_t pipe_smem_bytes(const SellView& v, size_t extra);
 unsigned pipe_grid(const zk_csr* A);
 
@@ -57,8 +57,6 @@ struct SolverBufs {
     bool jacobi, fma;
 };
 
-constexpr int kStashC = kBlock * sizeof(double2);  // 64 KiB complex stash
-constexpr int kStashR = kBlock * sizeof(double);   // 32 KiB real stash
 constexpr int kNodesPerBuf = 2 * 136;             // node slots per buffer (<= 129 nodes x NACC 2)
 constexpr int kNodeBytes = 2 * kNodesPerBuf * 16;  // double-buffered plan nodes
 constexpr int kRedThreads = 288;                   // 65 complex leaves x 4 lanes fit one pass
@@ -77,7 +75,6 @@ struct SolverPlan {
 
 namespace {
 
-using Sync = GroupSync<kConsumers>;
 
 __device__ __forceinline__ double2 neg(double2 a) { return make_double2(-a.x, -a.y); }
 
@@ -87,155 +84,29 @@ __device__ __forceinline__ void stop(SolverState* st, int32_t status, int32_t wh
     st->done = 1;
 }
 
-// Reduction ops over the stash of the block just computed (smem reads only).
-struct StashNorm2 {  // |b|^2, |r0|^2 (setup)
-    const double2* b;
-    const double2* stash;
-    int64_t base;
-    struct Item { double2 b; };
-    static constexpr int U = 4;
-    __device__ Item load(int64_t e) const { return {b[e]}; }
-    __device__ void apply(int64_t e, const Item& it, double (&v)[2]) const {
-        v[0] = abs2_np(it.b);
-        v[1] = abs2_np(stash[e - base]);
-    }
-};
-
-struct StashSelfDot {  // <r0, r0> (setup)
-    const double2* stash;
-    int64_t base;
-    bool fma;
-    struct Item {};
-    static constexpr int U = 1;
-    __device__ Item load(int64_t) const { return {}; }
-    __device__ void apply(int64_t e, const Item&, double2 (&v)[1]) const {
-        double2 r0 = stash[e - base];
-        v[0] = f1(conjz(r0), r0, fma);
-    }
-};
-
-
-// Reduction ops over a shared-memory stash ring of per-row terms.
-template <typename V, int NACC>
-struct StashOp {
-    const V* stash;  // element e of the block at ((e - base) & mask) * NACC
-    int64_t base;
-    int mask;
-    struct Item {};
-    static constexpr int U = 1;
-    __device__ Item load(int64_t) const { return {}; }
-    __device__ void apply(int64_t e, const Item&, V (&v)[NACC]) const {
-        const int64_t k = (e - base) & mask;
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) v[a] = stash[k * NACC + a];
-    }
-};
-
-// Windowed block reduction for the SpMV-phase kernels.  Rows deposit their
-// reduction terms in a stash ring; after every window (named barrier passed)
-// the leaves lying entirely in finished rows are summed (leaf_upto table),
-// and after the last one warp 0 combines the tree and finishes the block
-// while the other warps go on.  Per thread state; every consumer thread
-// makes the same calls.
-template <typename V, int NACC>
-struct WinRed {
-    const char* plan_full;
-    const char* plan_tail;
-    V* stash;
-    int mask;   // stash rows - 1
-    V* nodes;   // 2 buffers of kNodesPerBuf
-    int buf;
-    int done;   // leaves already summed for the current block
-    bool got_v0;
-    V v0[NACC];
-
-    __device__ __forceinline__ const char* plan(int64_t base, int64_t n) const {
-        return base + kBlock <= n ? plan_full : plan_tail;
-    }
-    __device__ __forceinline__ void put(int64_t row, const V (&val)[NACC]) {
-        const int64_t k = row & (kBlock - 1) & mask;
-#pragma unroll
-        for (int a = 0; a < NACC; ++a) stash[k * NACC + a] = val[a];
-    }
-    __device__ __forceinline__ void take_v0() {
-        if (!got_v0 && threadIdx.x == 0) {
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) v0[a] = stash[a];
-        }
-        got_v0 = true;
-    }
-    __device__ __forceinline__ void window(int64_t blk, int64_t n, int slices_done) {
-        const int64_t base = blk * kBlock;
-        const char* p = plan(base, n);
-        take_v0();
-        const int hi = plan_hdr(p)->leaf_upto[slices_done];
-        leaf_phase<V, NACC>(p, base + 1, StashOp<V, NACC>{stash, base, mask}, nodes + buf * kNodesPerBuf,
-                            kConsumers, done, hi);
-        done = hi;
-    }
-    // Returns true in warp 0 of the CTA that finished the last block.
-    __device__ __forceinline__ bool finish(int64_t blk, int64_t n, V* partials, unsigned int* counter,
-                                           unsigned int total) {
-        const int64_t base = blk * kBlock;
-        const char* p = plan(base, n);
-        take_v0();
-        V* nb = nodes + buf * kNodesPerBuf;
-        leaf_phase<V, NACC>(p, base + 1, StashOp<V, NACC>{stash, base, mask}, nb, kConsumers, done);
-        done = 0;
-        got_v0 = false;
-        buf ^= 1;
-        named_sync(1, kConsumers);
-        if ((threadIdx.x >> 5) != 0) return false;
-        V pw[NACC];
-        warp_tree<V, NACC>(p, nb, pw);
-        return warp_finish<V, NACC>(p, v0, pw, partials, blk, counter, total);
-    }
-};
+// ---- SpMV-phase bodies (zk_spmv.cuh reducer pipeline) ----------------------
+// Each body stores its row outputs and returns the row's reduction terms;
+// finish() receives the in-order folded totals [complex re/im pairs..., reals...]
+// in lane 0 of the reducer warp of the CTA that retired the last block.
 
 // ---- setup: r0 = b - A x0, ||b||, ||r0||, <r0, r0> (krylov.py:159-168, 255) ----
-// Runs once per solve; uses the plain (CTA-wide) block reduction.
 struct SetupBody {
-    static constexpr bool kReduce = true;
+    static constexpr int kNC = 1, kNR = 2, kSV = 1;  // staged: b
     SolverBufs B;
-    PlanPtrs pc, pr;
-    double2* stash;
-    char* nodes;
-    unsigned int* flag;
-    double* res;
-    struct RowCtx { double2 b; };
-    __device__ RowCtx prefetch(int64_t row) { return {B.b[row]}; }
-    __device__ void row(int64_t row, double2 ax, const RowCtx& c) {
-        const int64_t base = (row / kBlock) * kBlock;
-        double2 r0 = cadd(c.b, f1(make_double2(-1.0, 0.0), ax, B.fma));
+    __device__ void row(int64_t row, const double2 (&ax)[1], const double2 (&sv)[1], double2 (&tc)[1], double (&tr)[2]) {
+        const double2 b = sv[0];
+        const double2 r0 = cadd(b, f1(make_double2(-1.0, 0.0), ax[0], B.fma));
         B.r[row] = r0;
         B.rs[row] = r0;
-        stash[row - base] = r0;
+        tc[0] = f1(conjz(r0), r0, B.fma);
+        tr[0] = abs2_np(b);
+        tr[1] = abs2_np(r0);
     }
-    __device__ void window_done(int64_t, int) {}
-    __device__ void block_done(int64_t blk) {
-        const int64_t base = blk * kBlock;
-        double outr[2];
-        block_reduce<double, 2>(pr, B.n, kBlock, blk, StashNorm2{B.b, stash, base},
-                                reinterpret_cast<double*>(nodes), outr, Sync());
-        double2 outc[1];
-        block_reduce<double2, 1>(pc, B.n, kBlock, blk, StashSelfDot{stash, base, B.fma},
-                                 reinterpret_cast<double2*>(nodes), outc, Sync());
-        double* P = B.partials;
-        double2* PC = reinterpret_cast<double2*>(P + 2 * B.nblocks);
-        if (threadIdx.x == 0) {
-            P[2 * blk] = outr[0];
-            P[2 * blk + 1] = outr[1];
-            PC[blk] = outc[0];
-        }
+    __device__ void finish(const double* t) {  // [<r0,r0>.re, .im, |b|^2, |r0|^2]
         SolverState* st = B.st;
-        if (!arrive_last(&st->counter, (unsigned)B.nblocks, flag, Sync())) return;
-        double tr[2];
-        ordered_fold<double>(P, 2, B.nblocks, reinterpret_cast<double*>(stash), 4096, tr, res, Sync());
-        double2 tc;
-        ordered_fold<double2>(PC, 1, B.nblocks, stash, 2048, &tc, res, Sync());
-        if (threadIdx.x != 0) return;
         st->counter = 0;
-        const double bn = __dsqrt_rn(tr[0]), rn = __dsqrt_rn(tr[1]);
+        const double bn = __dsqrt_rn(t[2]), rn = __dsqrt_rn(t[3]);
+        const double2 tc = make_double2(t[0], t[1]);
         st->b_norm = bn;
         const double h0 = bn > 0.0 ? __ddiv_rn(rn, bn) : 0.0;
         B.hist[0] = h0;
@@ -261,18 +132,12 @@ struct SetupBody {
     }
 };
 
-__global__ void __launch_bounds__(kPipeThreads, 1) k_setup(SellView A, SolverBufs B, PlanPtrs pc, PlanPtrs pr) {
+__global__ void __launch_bounds__(kRedPipeThreads, 1) k_setup(SellView A, SolverBufs B, RedCfg R) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
     if (B.st->done) return;
-    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    SetupBody body{B, pc, pr, reinterpret_cast<double2*>(extra), reinterpret_cast<char*>(extra + kStashC), &s_flag,
-                   s_res};
-    sell_run(A, B.x, body, smem);
+    SetupBody body{B};
+    sell_run<1>(A, B.x, nullptr, body, R, smem);
 }
-
-__device__ __forceinline__ int stash_rows(const SellView& A) { return A.win < kBlock / kSlice ? kStashRows : kBlock; }
 
 // ---- K1: p update for the first iteration (p = v = 0) ----
 // p = ((p + F1(-w, v)) * beta) + F1(1, r); p^ = F1(p, minv)
@@ -306,114 +171,92 @@ __global__ void __launch_bounds__(256) k_p_next(SolverBufs B) {
         p_update(B, mw, beta, i, B.p[i], B.v[i], B.r[i], B.jacobi ? __ldg(B.minv + i) : make_double2(0.0, 0.0));
 }
 
-// ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
-struct PivotBody {
-    static constexpr bool kReduce = true;
-    SolverBufs B;
-    WinRed<double2, 1> red;
-    struct RowCtx { double2 rs; };
-    __device__ RowCtx prefetch(int64_t row) { return {__ldg(B.rs + row)}; }
-    __device__ void row(int64_t row, double2 av, const RowCtx& c) {
-        B.v[row] = av;
-        const double2 t[1] = {f1(conjz(c.rs), av, B.fma)};
-        red.put(row, t);
+// pivot = <r~, v> -> alpha (krylov.py:268-271); false when the loop stopped
+__device__ __forceinline__ void pivot_to_alpha(SolverState* st, double2 pivot) {
+    if (small_py(pivot)) {
+        stop(st, ST_BREAKDOWN, BD_PIVOT);
+        return;
     }
-    __device__ void window_done(int64_t blk, int j) { red.window(blk, B.n, j); }
-    __device__ void block_done(int64_t blk) {
-        double2* PC = reinterpret_cast<double2*>(B.partials);
-        if (!red.finish(blk, B.n, PC, &B.st->counter, (unsigned)B.nblocks)) return;
-        double2 pivot;
-        warp_fold<double2>(PC, 1, B.nblocks, red.stash, 1024, &pivot);
-        if ((threadIdx.x & 31) != 0) return;
+    st->alpha = cdiv_py(st->rho, pivot);
+}
+
+// ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
+// Last kernel of the loop body: sets the graph's WHILE condition (the
+// prologue instance, use_cond = 0, runs the first iteration's K2).
+struct PivotBody {
+    static constexpr int kNC = 1, kNR = 0, kSV = 1;  // staged: r~
+    SolverBufs B;
+    cudaGraphConditionalHandle cond;
+    int use_cond;
+    __device__ void row(int64_t row, const double2 (&av)[1], const double2 (&sv)[1], double2 (&tc)[1], double (&)[1]) {
+        B.v[row] = av[0];
+        tc[0] = f1(conjz(sv[0]), av[0], B.fma);
+    }
+    __device__ void finish(const double* t) {
         SolverState* st = B.st;
         st->counter = 0;
-        if (small_py(pivot)) {
-            stop(st, ST_BREAKDOWN, BD_PIVOT);
-            return;
-        }
-        st->alpha = cdiv_py(st->rho, pivot);
+        pivot_to_alpha(st, make_double2(t[0], t[1]));
+        if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
     }
 };
 
-__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_pivot(SellView A, SolverBufs B, PlanPtrs pc) {
+__global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_pivot(SellView A, SolverBufs B, RedCfg R,
+                                                                   cudaGraphConditionalHandle cond, int use_cond) {
     extern __shared__ __align__(128) unsigned char smem[];
-    SolverState* st = B.st;
-    if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;
-    if (st->done) return;
-    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    const int rows = stash_rows(A);
-    PivotBody body{B, {pc.full, pc.tail, reinterpret_cast<double2*>(extra), rows - 1,
-                       reinterpret_cast<double2*>(extra + rows * sizeof(double2)), 0, 0, false, {}}};
-    sell_run(A, B.ph, body, smem);
+    if (B.st->done) {
+        if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
+    PivotBody body{B, cond, use_cond};
+    sell_run<1>(A, B.ph, nullptr, body, R, smem);
 }
 
 // ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
 struct TBody {
-    static constexpr bool kReduce = true;
+    static constexpr int kNC = 2, kNR = 0, kSV = 1;  // staged: s
     SolverBufs B;
-    WinRed<double2, 2> red;
-    struct RowCtx { double2 s; };
-    __device__ RowCtx prefetch(int64_t row) { return {B.s[row]}; }
-    __device__ void row(int64_t row, double2 at, const RowCtx& c) {
-        B.t[row] = at;
-        const double2 ct = conjz(at);
-        const double2 t[2] = {f1(ct, at, B.fma), f1(ct, c.s, B.fma)};
-        red.put(row, t);
+    __device__ void row(int64_t row, const double2 (&at)[1], const double2 (&sv)[1], double2 (&tc)[2], double (&)[1]) {
+        B.t[row] = at[0];
+        const double2 ct = conjz(at[0]);
+        tc[0] = f1(ct, at[0], B.fma);
+        tc[1] = f1(ct, sv[0], B.fma);
     }
-    __device__ void window_done(int64_t blk, int j) { red.window(blk, B.n, j); }
-    __device__ void block_done(int64_t blk) {
-        double2* PC = reinterpret_cast<double2*>(B.partials);
-        if (!red.finish(blk, B.n, PC, &B.st->counter, (unsigned)B.nblocks)) return;
-        double2 tot[2];
-        warp_fold<double2>(PC, 2, B.nblocks, red.stash, 1024, tot);
-        if ((threadIdx.x & 31) != 0) return;
+    __device__ void finish(const double* t) {
         SolverState* st = B.st;
         st->counter = 0;
-        if (small_py(tot[0])) {
+        const double2 tt = make_double2(t[0], t[1]), ts = make_double2(t[2], t[3]);
+        if (small_py(tt)) {
             stop(st, ST_BREAKDOWN, BD_TT);
             return;
         }
-        const double2 w = cdiv_py(tot[1], tot[0]);
+        const double2 w = cdiv_py(ts, tt);
         st->omega = w;
         if (small_py(w)) stop(st, ST_BREAKDOWN, BD_OMEGA);
     }
 };
 
-__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_t(SellView A, SolverBufs B, PlanPtrs pc) {
+__global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_t(SellView A, SolverBufs B, RedCfg R) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (B.st->done) return;
-    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    const int rows = stash_rows(A);
-    TBody body{B, {pc.full, pc.tail, reinterpret_cast<double2*>(extra), rows - 1,
-                   reinterpret_cast<double2*>(extra + 2 * rows * sizeof(double2)), 0, 0, false, {}}};
-    sell_run(A, B.sh, body, smem);
+    TBody body{B};
+    sell_run<1>(A, B.sh, nullptr, body, R, smem);
 }
 
 // ---- true residual ||b + F1(-1, A x)|| / ||b|| (krylov.py:183-186) ----
-// MODE 0: on the s-check path (K6x);  MODE 1: end of iteration (K61).
+// MODE 0: on the s-check path (K6x, krylov.py:275-279);  MODE 1: end of
+// iteration (K61, krylov.py:288-294), which also runs the next iteration's
+// rho/omega breakdown checks (krylov.py:256-259).
 template <int MODE>
 struct ResBody {
-    static constexpr bool kReduce = true;
+    static constexpr int kNC = 0, kNR = 1, kSV = 1;  // staged: b
     SolverBufs B;
-    WinRed<double, 1> red;
-    cudaGraphConditionalHandle cond;
-    int use_cond;
-    struct RowCtx { double2 b; };
-    __device__ RowCtx prefetch(int64_t row) { return {B.b[row]}; }
-    __device__ void row(int64_t row, double2 ax, const RowCtx& c) {
-        const double2 rv = cadd(c.b, f1(make_double2(-1.0, 0.0), ax, B.fma));
-        const double t[1] = {abs2_np(rv)};
-        red.put(row, t);
+    __device__ void row(int64_t, const double2 (&ax)[1], const double2 (&sv)[1], double2 (&)[1], double (&tr)[1]) {
+        tr[0] = abs2_np(cadd(sv[0], f1(make_double2(-1.0, 0.0), ax[0], B.fma)));
     }
-    __device__ void window_done(int64_t blk, int j) { red.window(blk, B.n, j); }
-    __device__ void block_done(int64_t blk) {
-        if (!red.finish(blk, B.n, B.partials, &B.st->counter, (unsigned)B.nblocks)) return;
-        double rr;
-        warp_fold<double>(B.partials, 1, B.nblocks, red.stash, 2048, &rr);
-        if ((threadIdx.x & 31) != 0) return;
+    __device__ void finish(const double* t) {
         SolverState* st = B.st;
         st->counter = 0;
-        const double rel = __ddiv_rn(__dsqrt_rn(rr), st->b_norm);
+        const double rel = __ddiv_rn(__dsqrt_rn(t[0]), st->b_norm);
         if (MODE == 0) {
             if (rel <= st->tol) {
                 st->iterations++;
@@ -432,30 +275,20 @@ struct ResBody {
             stop(st, ST_CONVERGED, BD_NONE);
         } else if (st->iterations >= st->maxit) {
             stop(st, ST_NOT_CONVERGED, BD_NONE);
-        } else if (small_py(st->rho_old)) {  // next iteration's checks (krylov.py:256-259)
+        } else if (small_py(st->rho_old)) {
             stop(st, ST_BREAKDOWN, BD_RHO);
         } else if (small_py(st->omega)) {
             stop(st, ST_BREAKDOWN, BD_OMEGA);
         }
-        if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
     }
 };
 
 template <int MODE>
-__global__ void __launch_bounds__(kPipeThreads, 1) k_true_res(SellView A, SolverBufs B, PlanPtrs pr,
-                                                              cudaGraphConditionalHandle cond, int use_cond) {
+__global__ void __launch_bounds__(kRedPipeThreads, 1) k_true_res(SellView A, SolverBufs B, RedCfg R) {
     extern __shared__ __align__(128) unsigned char smem[];
-    SolverState* st = B.st;
-    if (st->done || (MODE == 0 && !st->scheck)) {
-        if (MODE == 1 && use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
-        return;
-    }
-    unsigned char* extra = smem + kBarBytes + (size_t)A.ns * A.stage_bytes;
-    const int rows = stash_rows(A);
-    ResBody<MODE> body{B, {pr.full, pr.tail, reinterpret_cast<double*>(extra), rows - 1,
-                           reinterpret_cast<double*>(extra + rows * sizeof(double)), 0, 0, false, {}},
-                       cond, use_cond};
-    sell_run(A, B.x, body, smem);
+    if (B.st->done || (MODE == 0 && !B.st->scheck)) return;
+    ResBody<MODE> body{B};
+    sell_run<1>(A, B.x, nullptr, body, R, smem);
 }
 
 // ---- persistent block-pass kernels for the fused level-1 phases ----------
@@ -514,6 +347,7 @@ struct SUpdateOp {
 __global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;  // loop-body executions (launch accounting)
     if (st->done) return;
     SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
     double* nodes = reinterpret_cast<double*>(smem + kFoldScratch);
@@ -607,16 +441,19 @@ void smem_attr(K kernel, size_t bytes) {
 struct Launch {
     zk_context* c;
     SolverPlan* P;
-    SellView As, Ap, At, Ar;                // ring geometry of setup, K2, K4, K6x/K61 (their stashes differ)
-    size_t smem_s, smem_p, smem_t, smem_r;  // dynamic smem of the SpMV-phase kernels
+    // ring geometry + dynamic smem of the SpMV-phase kernels (their reducer
+    // stashes and staged vectors differ): setup, K2, K4, K6x/K61
+    SellView As, Ap, At, Ar;
+    size_t smem_s, smem_p, smem_t, smem_r;
+    RedCfg red;
     PlanPtrs pc, pr;
     unsigned nb, ew, pg, rg;  // blocks, elementwise grid, SpMV grid, level-1 persistent grid
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
-// kernel and ev[k+1] after it (prologue phases 0-1, body phases 2-9).
+// kernel and ev[k+1] after it (prologue phases 0-2, body phases 3-10).
 struct PhaseEvents {
-    cudaEvent_t ev[11] = {};
+    cudaEvent_t ev[12] = {};
     bool on = false;
     void rec(int k, cudaStream_t s) {
         if (on) ZK_CUDA(cudaEventRecord(ev[k], s));
@@ -625,31 +462,36 @@ struct PhaseEvents {
 
 void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(0, s);
-    k_setup<<<L.pg, kPipeThreads, L.smem_s, s>>>(L.As, L.P->bufs, L.pc, L.pr);
+    k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, L.P->bufs, L.red);
     if (pe) pe->rec(1, s);
     k_p_first<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(2, s);
+    k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.red, 0, 0);
+    if (pe) pe->rec(3, s);
 }
+constexpr int kPrologueKernels = 3;
 
+// One iteration: K3, [K3x, K6x], K4, K5, K61, then the next iteration's Kp
+// and K2 (K61 first, so x is still in L2 when its SpMV gathers it).
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
-    if (pe) pe->rec(2, s);
-    k_spmv_pivot<<<L.pg, kPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.pc);
     if (pe) pe->rec(3, s);
     k_s_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
     if (pe) pe->rec(4, s);
     k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(5, s);
-    k_true_res<0><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, 0);
+    k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
     if (pe) pe->rec(6, s);
-    k_spmv_t<<<L.pg, kPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.pc);
+    k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.red);
     if (pe) pe->rec(7, s);
     k_xr_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
     if (pe) pe->rec(8, s);
-    k_p_next<<<L.ew, 256, 0, s>>>(L.P->bufs);
+    k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
     if (pe) pe->rec(9, s);
-    k_true_res<1><<<L.pg, kPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.pr, cond, use_cond);
+    k_p_next<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(10, s);
+    k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.red, cond, use_cond);
+    if (pe) pe->rec(11, s);
 }
 constexpr int kBodyKernels = 8;
 
@@ -710,6 +552,17 @@ void build_graph(const Launch& L) {
 }
 
 }  // namespace
+
+#if defined(ZK_EXP) && ZK_EXP >= 10
+void debug_read_solver(unsigned long long* out, bool reset) {
+    ZK_CUDA(cudaDeviceSynchronize());
+    ZK_CUDA(cudaMemcpyFromSymbol(out, zk_dbg, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {};
+        ZK_CUDA(cudaMemcpyToSymbol(zk_dbg, z, sizeof(z)));
+    }
+}
+#endif
 
 void destroy_solver_plan(zk_context* c, SolverPlan* P) {
     if (!P) return;
@@ -788,21 +641,24 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     Launch L;
     L.c = c;
     L.P = P;
-    // stash ring: kStashRows rows when the matrix has no long rows
-    // (windowed reductions), a whole 4096-row block otherwise
-    const size_t srows = A->n_long ? kBlock : kStashRows;
-    const size_t ex_p = srows * 16 + kNodeBytes, ex_t = 2 * srows * 16 + kNodeBytes, ex_r = srows * 8 + kNodeBytes;
-    L.As = sell_view(A, c, kStashC + kNodeBytes);
-    L.As.win = kBlock / kSlice;
-    L.Ap = sell_view(A, c, ex_p);
-    L.At = sell_view(A, c, ex_t);
-    L.Ar = sell_view(A, c, ex_r);
-    L.smem_s = pipe_smem_bytes(L.As, kStashC + kNodeBytes);
+    const size_t ex_s = RedSmem<1, 2>::kBytes, ex_p = RedSmem<1, 0>::kBytes, ex_t = RedSmem<2, 0>::kBytes,
+                 ex_r = RedSmem<0, 1>::kBytes;
+    L.As = sell_view(A, c, ex_s, 1);
+    L.As.sv[0] = B.b;
+    L.Ap = sell_view(A, c, ex_p, 1);
+    L.Ap.sv[0] = B.rs;
+    L.At = sell_view(A, c, ex_t, 1);
+    L.At.sv[0] = B.s;
+    L.Ar = sell_view(A, c, ex_r, 1);
+    L.Ar.sv[0] = B.b;
+    L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_p = pipe_smem_bytes(L.Ap, ex_p);
     L.smem_t = pipe_smem_bytes(L.At, ex_t);
     L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
+    unsigned int* ctr = &B.st->counter;
+    L.red = RedCfg{L.pc, L.pr, B.partials, ctr};
     L.nb = (unsigned)B.nblocks;
     L.pg = pipe_grid(A);
     L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
@@ -823,19 +679,19 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
             for (auto& e : pe.ev) ZK_CUDA(cudaEventCreate(&e));
         launch_prologue(L, s, &pe);
         ZK_CUDA(cudaGetLastError());
-        if (pe.on) accumulate(c, pe, 0, 1);
+        if (pe.on) accumulate(c, pe, 0, kPrologueKernels - 1);
         for (;;) {
             launch_body(L, s, 0, 0, &pe);
             ZK_CUDA(cudaGetLastError());
             ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
             ZK_CUDA(cudaStreamSynchronize(s));
-            if (pe.on) accumulate(c, pe, 2, 9);
+            if (pe.on) accumulate(c, pe, kPrologueKernels, kPrologueKernels + kBodyKernels - 1);
             if (out.done) break;
         }
         if (pe.on)
             for (auto& e : pe.ev) cudaEventDestroy(e);
     }
-    c->launches += 2 + kBodyKernels * out.trips;
+    c->launches += kPrologueKernels + kBodyKernels * out.trips;
     const int64_t it = out.iterations;
     ZK_CUDA(cudaMemcpyAsync(history_host, B.hist, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost, s));
     if (out.trivial_zero) ZK_CUDA(cudaMemsetAsync(x_out, 0, vb, s));
@@ -846,7 +702,7 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     rep->breakdown = out.status == ST_BREAKDOWN ? out.what : 0;
     rep->final_relative_residual = history_host[it];
     rep->history_len = it + 1;
-    rep->kernel_launches = 2 + kBodyKernels * out.trips;
+    rep->kernel_launches = kPrologueKernels + kBodyKernels * out.trips;
     return out.status == ST_BREAKDOWN ? ZK_ERR_BREAKDOWN : ZK_OK;
 }
 

@@ -112,6 +112,89 @@ __device__ __forceinline__ void leaf_phase(const char* plan, int64_t seg0, const
     }
 }
 
+// Leaf phase run by a single warp over leaves [leaf_lo, leaf_hi) (the
+// reducer warp of the SpMV pipelines); same item mapping and order as
+// leaf_phase with the warp's lane as the thread index.
+template <typename V, int NACC, class Op>
+__device__ __forceinline__ void warp_leaves(const char* plan, int64_t seg0, const Op& op, V* nodes, int leaf_lo,
+                                            int leaf_hi) {
+    constexpr int LANES = VT<V>::lanes;
+    const PlanHeader* h = plan_hdr(plan);
+    const int L = h->L;
+    const int lane = threadIdx.x & 31;
+    if (L <= 0) return;
+    if (leaf_hi > h->nleaves) leaf_hi = h->nleaves;
+    if (leaf_lo >= leaf_hi) return;
+    if (h->seq) {
+        if (lane == 0) {
+            V s[NACC];
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) s[a] = VT<V>::negzero();
+            for (int k = 0; k < L; ++k) {
+                V v[NACC];
+                typename Op::Item it = op.load(seg0 + k);
+                op.apply(seg0 + k, it, v);
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) s[a] = VT<V>::add(s[a], v[a]);
+            }
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) nodes[a] = s[a];
+        }
+        return;
+    }
+    const int2* leaves = reinterpret_cast<const int2*>(plan + h->leaves_off);
+    const int nitems = leaf_hi * LANES;
+    const int q = lane & (LANES - 1);
+    for (int it0 = leaf_lo * LANES; it0 < nitems; it0 += 32) {
+        const int itm = it0 + lane;
+        const bool valid = itm < nitems;
+        const int leaf = itm / LANES;
+        const int2 lf = valid ? __ldg(leaves + leaf) : make_int2(0, 0);
+        const int G = lf.y / LANES;
+        const int rem = lf.y - G * LANES;
+        const int64_t e0 = seg0 + lf.x + q;
+        V acc[NACC];
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) acc[a] = VT<V>::zero();
+        if (valid) {
+            for (int g = 0; g < G; ++g) {
+                V v[NACC];
+                op.apply(e0 + (int64_t)LANES * g, typename Op::Item{}, v);
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) acc[a] = (g == 0) ? v[a] : VT<V>::add(acc[a], v[a]);
+            }
+        }
+#pragma unroll
+        for (int d = 1; d < LANES; d <<= 1) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) {
+                V o = VT<V>::shfl_down(acc[a], d);
+                if ((q & (2 * d - 1)) == 0) acc[a] = VT<V>::add(acc[a], o);
+            }
+        }
+        V left[NACC];
+        if (valid && q < rem) {
+            op.apply(seg0 + lf.x + (int64_t)LANES * G + q, typename Op::Item{}, left);
+        } else {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) left[a] = VT<V>::zero();
+        }
+        const int grp = lane & ~(LANES - 1);
+#pragma unroll
+        for (int j = 0; j < LANES - 1; ++j) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) {
+                V o = VT<V>::shfl(left[a], grp + j);
+                if (j < rem) acc[a] = VT<V>::add(acc[a], o);
+            }
+        }
+        if (valid && q == 0) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) nodes[leaf * NACC + a] = acc[a];
+        }
+    }
+}
+
 // One full warp combines the leaves (after a barrier made them visible).
 // Every lane returns PW of the segment in `pw` (untouched when L == 0).
 template <typename V, int NACC>

@@ -64,6 +64,7 @@ struct zk_csr {
     double2* aa;                    // [sell_elems]
     int32_t* ja;                    // [sell_elems]
     int64_t* slice_off;             // [nslices + 1]
+    int32_t* slice_cmax;            // [nslices] largest column index of the slice (-1: none)
     uint8_t* rowlen;                // [nslices * 32]; 255 = long row
     int32_t n_long;
     int32_t* long_row;              // [n_long]

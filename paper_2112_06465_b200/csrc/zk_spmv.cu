@@ -11,8 +11,9 @@ namespace zk {
 
 // Ring geometry for a launch that also needs `extra` bytes of dynamic
 // shared memory after the ring (epilogue stash, reduction nodes).
-SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
+SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) {
     SellView v;
+    v.sv[0] = v.sv[1] = nullptr;
     v.n_rows = A->n_rows;
     v.n_cols = A->n_cols;
     v.nslices = A->nslices;
@@ -20,6 +21,7 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
     v.aa = A->aa;
     v.ja = A->ja;
     v.slice_off = A->slice_off;
+    v.slice_cmax = A->slice_cmax;
     v.rowlen = A->rowlen;
     v.long_row = A->long_row;
     v.long_blk_ptr = A->n_long ? A->long_blk_ptr : nullptr;
@@ -28,9 +30,13 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
     v.long_aa = A->long_aa;
     // Ring chunk = (1 + 4 cm) columns of a slice (two pairwise groups, or one
     // when shared memory is tight), independent of the row width.
-    v.win = A->n_long ? kBlock / kSlice : kWindowSlices;
     const int w = A->wmax > 0 ? A->wmax : 1;
-    const long avail = (long)kSmemLimit - 1024 - kBarBytes - (long)extra;
+    // Stay within the 196 KB shared-memory carve-out so that L1 keeps >= 60 KB
+    // for the x gathers (a 228 KB carve-out leaves 28 KB and the gathers'
+    // L1 hit rate collapses); ZK_SMEM_KB overrides (experiments only).
+    const char* env_kb = std::getenv("ZK_SMEM_KB");
+    const long limit = env_kb ? std::atol(env_kb) * 1024 : 196 * 1024;
+    const long avail = std::min<long>(limit, kSmemLimit) - 1024 - kBarBytes - (long)extra;
     const char* env_cm = std::getenv("ZK_CM");      // tuning overrides (experiments only)
     const char* env_ns = std::getenv("ZK_NS");
     const int cm_hi = env_cm ? std::atoi(env_cm) : 2;
@@ -43,7 +49,9 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
         v.nch = 1;
         v.ja_off = wpad * kSlice * 16;
         v.rl_off = v.ja_off + wpad * kSlice * 4;
-        v.stage_bytes = (v.rl_off + kSlice + 127) / 128 * 128;
+        v.sv_off = v.rl_off + kSlice;
+        v.nsv = nsv;
+        v.stage_bytes = (v.sv_off + nsv * kSlice * 16 + 127) / 128 * 128;
         const long ns = avail / v.stage_bytes;
         const long cap = std::max<long>(10, 180 * 1024 / v.stage_bytes);  // deeper rings measured slower on C4
         v.ns = (int)(ns > std::min<long>(cap, kMaxStages) ? std::min<long>(cap, kMaxStages) : (ns < 1 ? 1 : ns));
@@ -59,6 +67,8 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra) {
         v.nch = w <= cols ? 1 : 1 + (w - cols + 4 * cm - 1) / (4 * cm);
         v.ja_off = cols * kSlice * 16;
         v.rl_off = 0;
+        v.sv_off = 0;
+        v.nsv = nsv;
         v.stage_bytes = (cols * kSlice * 20 + 127) / 128 * 128;
         const long ns = avail / v.stage_bytes;
         v.ns = (int)(ns > kMaxStages ? kMaxStages : (ns < 1 ? 1 : ns));
@@ -89,7 +99,8 @@ namespace {
 __global__ void k_sell_scatter(int64_t n_rows, int64_t n_cols, const int64_t* __restrict__ ia,
                                const int64_t* __restrict__ ja, const double2* __restrict__ aa,
                                const int64_t* __restrict__ slice_off, const uint8_t* __restrict__ rowlen,
-                               double2* __restrict__ saa, int32_t* __restrict__ sja, unsigned int* bad) {
+                               double2* __restrict__ saa, int32_t* __restrict__ sja, int32_t* __restrict__ cmax,
+                               unsigned int* bad) {
     const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= n_rows) return;
     const int len = rowlen[row];
@@ -104,12 +115,14 @@ __global__ void k_sell_scatter(int64_t n_rows, int64_t n_cols, const int64_t* __
         sja[base + 32 * (int64_t)k] = ok ? (int32_t)j : 0;
     }
     if (!ok) atomicOr(bad, 1u);
+    if (len > 0 && ok) atomicMax(cmax + row / kSlice, (int32_t)ja[lo + len - 1]);  // columns ascend
 }
 
 __global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __restrict__ long_row,
                                const int64_t* __restrict__ ia, const int64_t* __restrict__ ja,
                                const double2* __restrict__ aa, const int64_t* __restrict__ long_ia,
-                               int32_t* __restrict__ lja, double2* __restrict__ laa, unsigned int* bad) {
+                               int32_t* __restrict__ lja, double2* __restrict__ laa, int32_t* __restrict__ cmax,
+                               unsigned int* bad) {
     const int li = blockIdx.x * blockDim.x + threadIdx.x;
     if (li >= n_long) return;
     const int64_t lo = ia[long_row[li]], len = long_ia[li + 1] - long_ia[li];
@@ -121,23 +134,25 @@ __global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __
         laa[long_ia[li] + k] = aa[lo + k];
     }
     if (!ok) atomicOr(bad, 1u);
+    if (len > 0 && ok) atomicMax(cmax + long_row[li] / kSlice, (int32_t)ja[lo + len - 1]);
 }
 
 struct PlainSpmv {
-    static constexpr bool kReduce = false;
+    static constexpr int kNC = 0, kNR = 0, kSV = 0;  // no reductions, no staged operands
     double2* __restrict__ y;
-    struct RowCtx {};
-    __device__ __forceinline__ RowCtx prefetch(int64_t) { return {}; }
-    __device__ __forceinline__ void row(int64_t r, double2 v, const RowCtx&) { y[r] = v; }
-    __device__ __forceinline__ void window_done(int64_t, int) {}
-    __device__ __forceinline__ void block_done(int64_t) {}
+    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[1], const double2 (&)[1], double2 (&)[1],
+                                        double (&)[1]) {
+        y[r] = v[0];
+    }
+    __device__ __forceinline__ void finish(const double*) {}
 };
 
 __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv(SellView A, const double2* __restrict__ x,
                                                           double2* __restrict__ y) {
     extern __shared__ __align__(128) unsigned char smem[];
     PlainSpmv body{y};
-    sell_run(A, x, body, smem);
+    const RedCfg R{};
+    sell_run<1>(A, x, nullptr, body, R, smem);
 }
 
 template <class T>
@@ -149,7 +164,7 @@ T* dalloc(zk_context* c, size_t count) {
 
 void destroy_sell(zk_csr* A) {
     zk_context* c = A->ctx;
-    void* ptrs[] = {A->aa, A->ja, A->slice_off, A->rowlen, A->long_row, A->long_blk_ptr,
+    void* ptrs[] = {A->aa, A->ja, A->slice_off, A->slice_cmax, A->rowlen, A->long_row, A->long_blk_ptr,
                     A->long_ia, A->long_ja, A->long_aa};
     for (void* p : ptrs)
         if (p) c->alloc.free(p);
@@ -200,6 +215,8 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
     A->aa = dalloc<double2>(c, A->sell_elems);
     A->ja = dalloc<int32_t>(c, A->sell_elems);
     A->slice_off = dalloc<int64_t>(c, A->nslices + 1);
+    A->slice_cmax = dalloc<int32_t>(c, A->nslices);
+    ZK_CUDA(cudaMemsetAsync(A->slice_cmax, 0xff, sizeof(int32_t) * (A->nslices ? A->nslices : 1), st));
     A->rowlen = dalloc<uint8_t>(c, nrp);
     ZK_CUDA(cudaMemsetAsync(A->aa, 0, sizeof(double2) * A->sell_elems, st));
     ZK_CUDA(cudaMemsetAsync(A->ja, 0, sizeof(int32_t) * A->sell_elems, st));
@@ -209,7 +226,7 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
     if (n_rows > 0) {
         k_sell_scatter<<<(unsigned)((n_rows + 255) / 256), 256, 0, st>>>(n_rows, n_cols, ia_d, ja_d, aa_d,
                                                                          A->slice_off, A->rowlen, A->aa, A->ja,
-                                                                         c->counter + 1);
+                                                                         A->slice_cmax, c->counter + 1);
         ZK_CUDA(cudaGetLastError());
         c->launches++;
     }
@@ -225,7 +242,8 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
         ZK_CUDA(cudaMemcpyAsync(A->long_ia, long_ia.data(), sizeof(int64_t) * long_ia.size(), cudaMemcpyHostToDevice,
                                 st));
         k_long_scatter<<<(A->n_long + 255) / 256, 256, 0, st>>>(A->n_long, n_cols, A->long_row, ia_d, ja_d, aa_d,
-                                                               A->long_ia, A->long_ja, A->long_aa, c->counter + 1);
+                                                               A->long_ia, A->long_ja, A->long_aa, A->slice_cmax,
+                                                               c->counter + 1);
         ZK_CUDA(cudaGetLastError());
         c->launches++;
     }
@@ -241,13 +259,27 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
     return A;
 }
 
+#if defined(ZK_EXP) && ZK_EXP >= 10
+void debug_read_spmv(unsigned long long* out, bool reset) {
+    ZK_CUDA(cudaDeviceSynchronize());
+    ZK_CUDA(cudaMemcpyFromSymbol(out, zk_dbg, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {};
+        ZK_CUDA(cudaMemcpyToSymbol(zk_dbg, z, sizeof(z)));
+    }
+}
+#endif
+
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
     if (A->n_rows == 0) return;
     if (A->nnz == 0) {
         ZK_CUDA(cudaMemsetAsync(y, 0, sizeof(double2) * A->n_rows, c->stream));
         return;
     }
-    SellView v = sell_view(A, c, 0);
+    const char* e_nsv = std::getenv("ZK_EXP_NSV");  // experiment: stage x rows with every slice
+    const int nsv = e_nsv ? std::atoi(e_nsv) : 0;
+    SellView v = sell_view(A, c, 0, nsv);
+    v.sv[0] = v.sv[1] = x;
     const size_t smem = pipe_smem_bytes(v, 0);
     ZK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_spmv<<<pipe_grid(A), kPipeThreads, smem, c->stream>>>(v, x, y);

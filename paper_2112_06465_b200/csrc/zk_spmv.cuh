@@ -31,27 +31,52 @@
 #pragma once
 #include "zk_common.cuh"
 #include "zk_pipe.cuh"
+#include "zk_blockred.cuh"
 
 namespace zk {
 
-constexpr int kConsumerWarps = 7;  // + 1 producer = 8 warps: 2 per SMSP, so up to 255 registers/thread
-constexpr int kConsumers = kConsumerWarps * 32;  // 256
-constexpr int kPipeThreads = kConsumers + 32;    // + producer warp
+// 8 warps per CTA (2 per SM sub-partition, so up to 255 registers/thread):
+// plain SpMV = 7 consumer warps + the TMA producer; fused reductions = 6
+// consumer warps + producer + reducer (a 9th warp would cap registers at 168).
+#ifndef ZK_RED_CW
+#define ZK_RED_CW 6
+#endif
+#ifndef ZK_B1
+#define ZK_B1 28
+#endif
+#ifndef ZK_PLAIN_CW
+#define ZK_PLAIN_CW 7
+#endif
+constexpr int kPipeThreads = 32 * (ZK_PLAIN_CW + 1);
+constexpr int kRedPipeThreads = 32 * (ZK_RED_CW + 2);
+template <bool RED> struct PipeWarps {
+    static constexpr int consumers = RED ? ZK_RED_CW : ZK_PLAIN_CW;
+    static constexpr int producer = consumers;
+    static constexpr int reducer = consumers + 1;
+};
 constexpr int kMaxStages = 32;
 constexpr int kBarBytes = 2 * kMaxStages * 8 + 2 * kMaxStages * 4;  // full, empty mbarriers + stage tags, widths
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kFullCols = 33;  // widest row handled by the whole-row prefetch path
-// Reduction windows: 28 slices (4 per consumer warp, 896 rows).  With a
-// 2048-row stash ring a window never overwrites rows a pending leaf (<= 128
-// elements) or the previous window's leaf pass still reads (896*2+128 < 2048).
-constexpr int kWindowSlices = 4 * kConsumerWarps;
-constexpr int kStashRows = 2048;
+// Reduction stash: a ring of kStashSlices slice slots (32 rows each) of
+// per-row reduction terms between the consumer warps and the reducer warp.
+constexpr int kStashSlices = 32;
+constexpr int kStashMask = kStashSlices * kSlice - 1;
+constexpr int kNodeSlots = 136;  // >= plan nodes (<= 129) per accumulator
+
+#if defined(ZK_EXP) && ZK_EXP >= 10
+static __device__ unsigned long long zk_dbg[16];  // per translation unit
+#if ZK_EXP >= 11
+__shared__ long long zk_dbg_sh[32];
+#endif
+#endif
 
 struct SellView {
     int64_t n_rows, n_cols, nslices, nblocks;
     const double2* __restrict__ aa;
     const int32_t* __restrict__ ja;
     const int64_t* __restrict__ slice_off;
+    const int32_t* __restrict__ slice_cmax;  // largest column of each slice (x leading edge)
     const uint8_t* __restrict__ rowlen;
     const int32_t* __restrict__ long_row;
     const int32_t* __restrict__ long_blk_ptr;
@@ -63,9 +88,11 @@ struct SellView {
     int32_t stage_bytes;  // (1 + 4 cm) columns x 32 rows x 20 B, 128 B rounded
     int32_t ja_off;       // byte offset of the column indices inside a stage
     int32_t rl_off;       // byte offset of the slice's 32 row lengths inside a stage (cm == 0)
+    int32_t sv_off;       // byte offset of the staged vector rows (cm == 0): nsv x 32 double2
+    int32_t nsv;          // vectors staged with each slice (the row epilogue's operands)
+    const double2* sv[2]; // their base pointers (row-indexed, n_rows long)
     int32_t ns;           // ring stages for this launch
     uint32_t ns_magic;    // floor(2^32 / ns) + 1: i / ns = umulhi(i, ns_magic) for i < 2^27
-    int32_t win;          // slices per reduction window (kWindowSlices, or a whole block with long rows)
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
 };
@@ -212,7 +239,7 @@ __device__ __forceinline__ double2 long_prod(const SellView& A, const double2* _
 // numpy CDOUBLE_pairwise_sum over products [s, s+L) of the side CSR,
 // evaluated iteratively (explicit post-order stack; no device recursion, so
 // the calling kernels keep their register allocation).
-static __device__ __noinline__ double2 long_pw(const SellView& A, const double2* __restrict__ x, int64_t s, int64_t L) {
+static __device__ __noinline__ double2 long_pw(const SellView A, const double2* __restrict__ x, int64_t s, int64_t L) {
     int64_t fs[40], fl[40];
     int8_t fphase[40];
     double2 vals[40];
@@ -280,35 +307,25 @@ __device__ __forceinline__ double2 prod_fma(double2 a, double2 xv) {
     return SWAP ? f1(xv, a, true) : f1(a, xv, true);
 }
 
-template <int W4, bool SWAP>
-__device__ __forceinline__ double2 row_fast(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
-                                            int lane, int len) {
-    constexpr int B1 = W4 < 28 ? W4 : 28;  // gathers in flight per batch (register budget)
-    const double2 z = make_double2(0.0, 0.0);
-    const int L = len - 1;
-    const int G = L >> 2;
-    const int rem = L - 4 * G;
-    double2 r[4] = {z, z, z, z}, lo[3] = {z, z, z};
-    double2 v0 = z;
-    double2 xs[B1];
+struct RowSum {
+    double2 v0, r[4], lo[3];
+    int G, rem, len;
+    __device__ __forceinline__ void init(int n) {
+        const double2 z = make_double2(0.0, 0.0);
+        len = n;
+        const int L = n - 1;
+        G = L >> 2;
+        rem = L - 4 * G;
+        v0 = z;
 #pragma unroll
-    for (int k = 0; k < B1; ++k) {
-        xs[k] = z;
-        if (k < len) xs[k] = __ldg(x + sja[32 * k + lane]);
+        for (int q = 0; q < 4; ++q) r[q] = z;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) lo[q] = z;
     }
-#pragma unroll
-    for (int k = 0; k < W4; ++k) {
-        if (k == B1) {  // second batch (rows wider than 28)
-#pragma unroll
-            for (int t = 0; t < W4 - B1; ++t) {
-                xs[t] = z;
-                if (B1 + t < len) xs[t] = __ldg(x + sja[32 * (B1 + t) + lane]);
-            }
-        }
-        const double2 p = prod_fma<SWAP>(saa[32 * k + lane], xs[k < B1 ? k : k - B1]);
+    __device__ __forceinline__ void add(int k, double2 p) {  // k: compile-time after unrolling
         if (k == 0) {
             v0 = p;
-            continue;
+            return;
         }
         const int g = (k - 1) >> 2, q = (k - 1) & 3;
         if (g < G) {
@@ -317,46 +334,507 @@ __device__ __forceinline__ double2 row_fast(const double2* __restrict__ x, const
             lo[q] = p;
         }
     }
-    double2 s = make_double2(-0.0, -0.0);
-    if (G > 0) s = cadd(cadd(r[0], r[1]), cadd(r[2], r[3]));
-    if (rem > 0) s = cadd(s, lo[0]);
-    if (rem > 1) s = cadd(s, lo[1]);
-    if (rem > 2) s = cadd(s, lo[2]);
-    if (len <= 0) return z;
-    if (len == 1) return v0;
-    return cadd(v0, s);
+    __device__ __forceinline__ double2 result() const {
+        double2 s = make_double2(-0.0, -0.0);
+        if (G > 0) s = cadd(cadd(r[0], r[1]), cadd(r[2], r[3]));
+        if (rem > 0) s = cadd(s, lo[0]);
+        if (rem > 1) s = cadd(s, lo[1]);
+        if (rem > 2) s = cadd(s, lo[2]);
+        if (len <= 0) return make_double2(0.0, 0.0);
+        if (len == 1) return v0;
+        return cadd(v0, s);
+    }
+};
+
+// Columns [K0, K1) of one vector: gathers first, then the products in order.
+template <int K0, int K1, bool SWAP>
+__device__ __forceinline__ void row_seg(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                        int lane, RowSum& acc) {
+    double2 xs[K1 - K0];
+#pragma unroll
+    for (int k = K0; k < K1; ++k) {
+        xs[k - K0] = make_double2(0.0, 0.0);
+        if (k < acc.len) xs[k - K0] = __ldg(x + sja[32 * k + lane]);
+    }
+#pragma unroll
+    for (int k = K0; k < K1; ++k) acc.add(k, prod_fma<SWAP>(saa[32 * k + lane], xs[k - K0]));
+}
+
+// ---- uniform slices: every row of the warp has exactly W entries --------
+// (the common case for stencil and FE matrices).  L, G and the leftover
+// count are compile-time constants, so the numpy order is straight-line
+// code with no predication at all.
+template <int K0, int K1, int W, bool SWAP>
+__device__ __forceinline__ void uni_seg(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                        int lane, double2& v0, double2 (&r)[4], double2 (&lo)[3]) {
+    constexpr int L = W - 1, G = L >> 2;
+    double2 xs[K1 - K0];
+#pragma unroll
+    for (int k = K0; k < K1; ++k) xs[k - K0] = __ldg(x + sja[32 * k + lane]);
+#if defined(ZK_EXP) && ZK_EXP >= 11
+    if (K0 == 0 && lane == 0) zk_dbg_sh[(threadIdx.x >> 5) * 2] = clock64();
+#endif
+#pragma unroll
+    for (int k = K0; k < K1; ++k) {
+        const double2 p = prod_fma<SWAP>(saa[32 * k + lane], xs[k - K0]);
+#if defined(ZK_EXP) && ZK_EXP >= 11
+        if (k == 0) {
+            double px = p.x;
+            asm volatile("" : "+d"(px));
+            if (lane == 0 && px != 12345.678) zk_dbg_sh[(threadIdx.x >> 5) * 2 + 1] = clock64();
+        }
+#endif
+        if (k == 0) {
+            v0 = p;
+        } else {
+            const int g = (k - 1) >> 2, q = (k - 1) & 3;
+            if (g < G) r[q] = (g == 0) ? p : cadd(r[q], p);
+            else lo[q] = p;
+        }
+    }
+}
+
+template <int K0, int W, bool SWAP>
+__device__ __forceinline__ void uni_segs(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                         int lane, double2& v0, double2 (&r)[4], double2 (&lo)[3]) {
+    constexpr int K1 = (K0 + ZK_B1 < W) ? K0 + ZK_B1 : W;
+    uni_seg<K0, K1, W, SWAP>(x, saa, sja, lane, v0, r, lo);
+    if constexpr (K1 < W) uni_segs<K1, W, SWAP>(x, saa, sja, lane, v0, r, lo);
+}
+
+template <int W, bool SWAP>
+__device__ __forceinline__ double2 row_uniform(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                               int lane) {
+    constexpr int L = W - 1, G = L >> 2, REM = L - 4 * G;
+    double2 v0, r[4], lo[3];
+    uni_segs<0, W, SWAP>(x, saa, sja, lane, v0, r, lo);
+    if constexpr (W == 1) {
+        return v0;
+    } else {
+        double2 s = make_double2(-0.0, -0.0);
+        if constexpr (G > 0) s = cadd(cadd(r[0], r[1]), cadd(r[2], r[3]));
+#pragma unroll
+        for (int j = 0; j < REM; ++j) s = cadd(s, lo[j]);
+        return cadd(v0, s);
+    }
 }
 
 template <bool SWAP>
-__device__ __forceinline__ double2 row_fast_dispatch(int W, const double2* __restrict__ x, const double2* saa,
-                                                     const int32_t* sja, int lane, int len) {
+__device__ __forceinline__ double2 row_uniform_dispatch(int W, const double2* __restrict__ x, const double2* saa,
+                                                        const int32_t* sja, int lane) {
+    switch (W) {
+#define ZK_UNI(w) \
+    case w: return row_uniform<w, SWAP>(x, saa, sja, lane);
+        ZK_UNI(1) ZK_UNI(2) ZK_UNI(3) ZK_UNI(4) ZK_UNI(5) ZK_UNI(6) ZK_UNI(7) ZK_UNI(8)
+        ZK_UNI(9) ZK_UNI(10) ZK_UNI(11) ZK_UNI(12) ZK_UNI(13) ZK_UNI(14) ZK_UNI(15) ZK_UNI(16)
+        ZK_UNI(17) ZK_UNI(18) ZK_UNI(19) ZK_UNI(20) ZK_UNI(21) ZK_UNI(22) ZK_UNI(23) ZK_UNI(24)
+        ZK_UNI(25) ZK_UNI(26) ZK_UNI(27) ZK_UNI(28) ZK_UNI(29) ZK_UNI(30) ZK_UNI(31) ZK_UNI(32)
+#undef ZK_UNI
+        default: return make_double2(0.0, 0.0);
+    }
+}
+
+// Columns [K0, W4) in batches of ZK_B1 gathers.
+template <int K0, int W4, bool SWAP>
+__device__ __forceinline__ void row_segs(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                         int lane, RowSum& acc) {
+    constexpr int K1 = (K0 + ZK_B1 < W4) ? K0 + ZK_B1 : W4;
+    row_seg<K0, K1, SWAP>(x, saa, sja, lane, acc);
+    if constexpr (K1 < W4) row_segs<K1, W4, SWAP>(x, saa, sja, lane, acc);
+}
+
+// NX = 1: out[0] = row of A x0.  NX = 2: out[1] = row of A x1 as well, the
+// second vector's row summed after the first (one register set for the
+// gathers: the two sets in flight at once spill at 255 registers).
+template <int NX>
+struct RowVals {
+    double2 v[NX];
+};
+
+template <int W4, bool SWAP>
+__device__ __forceinline__ double2 row_one(const double2* __restrict__ x, const double2* saa, const int32_t* sja,
+                                           int lane, int len) {
+    RowSum acc;
+    acc.init(len);
+    row_segs<0, W4, SWAP>(x, saa, sja, lane, acc);
+    return acc.result();
+}
+
+template <int W4, bool SWAP, int NX>
+__device__ __forceinline__ RowVals<NX> row_fast(const double2* __restrict__ x0, const double2* __restrict__ x1,
+                                                const double2* saa, const int32_t* sja, int lane, int len) {
+    RowVals<NX> out;
+    if constexpr (NX == 1) {
+        out.v[0] = row_one<W4, SWAP>(x0, saa, sja, lane, len);
+    } else {
+        // one code copy, run once per vector (the two rows' gather sets in
+        // flight together do not fit in 255 registers)
+#pragma unroll 1
+        for (int v = 0; v < 2; ++v) {
+            const double2 r = row_one<W4, SWAP>(v == 0 ? x0 : x1, saa, sja, lane, len);
+            if (v == 0) out.v[0] = r;
+            else out.v[1] = r;
+        }
+    }
+    return out;
+}
+
+template <bool SWAP, int NX>
+__device__ __forceinline__ RowVals<NX> row_fast_dispatch(int W, const double2* __restrict__ x0,
+                                                         const double2* __restrict__ x1, const double2* saa,
+                                                         const int32_t* sja, int lane, int len, bool pad) {
+    // pad: row beyond n_rows (its result is not used)
+    if (W >= 1 && W <= 32 && __all_sync(0xffffffffu, pad || len == W)) {
+        RowVals<NX> out;
+#pragma unroll 1
+        for (int v = 0; v < NX; ++v) {
+            const double2 r = row_uniform_dispatch<SWAP>(W, v == 0 ? x0 : x1, saa, sja, lane);
+            if (v == 0) out.v[0] = r;
+            else out.v[NX - 1] = r;
+        }
+        return out;
+    }
     switch ((W + 3) >> 2) {
         case 0:
-        case 1: return row_fast<4, SWAP>(x, saa, sja, lane, len);
-        case 2: return row_fast<8, SWAP>(x, saa, sja, lane, len);
-        case 3: return row_fast<12, SWAP>(x, saa, sja, lane, len);
-        case 4: return row_fast<16, SWAP>(x, saa, sja, lane, len);
-        case 5: return row_fast<20, SWAP>(x, saa, sja, lane, len);
-        case 6: return row_fast<24, SWAP>(x, saa, sja, lane, len);
-        case 7: return row_fast<28, SWAP>(x, saa, sja, lane, len);
-        case 8: return row_fast<32, SWAP>(x, saa, sja, lane, len);
-        default: return row_fast<36, SWAP>(x, saa, sja, lane, len);
+        case 1: return row_fast<4, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 2: return row_fast<8, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 3: return row_fast<12, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 4: return row_fast<16, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 5: return row_fast<20, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 6: return row_fast<24, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 7: return row_fast<28, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        case 8: return row_fast<32, SWAP, NX>(x0, x1, saa, sja, lane, len);
+        default: return row_fast<36, SWAP, NX>(x0, x1, saa, sja, lane, len);
+    }
+}
+
+// Index of long row `row` in the side CSR (binary search in its block's range).
+__device__ __forceinline__ int long_index(const SellView& A, int64_t blk, int64_t row) {
+    int lo = A.long_blk_ptr[blk], hi = A.long_blk_ptr[blk + 1] - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((int64_t)A.long_row[mid] < row) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Generic slice path (rows wider than kFullCols split over chunks, or the
+// non-FMA fingerprint): RowAcc per vector, chunk by chunk.  Out of line so
+// its registers do not weigh on the fast path.
+template <int NX>
+__device__ __noinline__ RowVals<NX> generic_slice(const SellView A, const double2* __restrict__ x0,
+                                                  const double2* __restrict__ x1, uint64_t* full, uint64_t* empty,
+                                                  volatile uint32_t* tag, const unsigned char* ring, uint32_t sq,
+                                                  int lane, int len) {
+    RowAcc acc[NX];
+#pragma unroll
+    for (int v = 0; v < NX; ++v) acc[v].init(len);
+    const int ns = A.ns, nch = A.nch;
+    for (int c = 0; c < nch; ++c) {
+        const uint32_t i = sq * (uint32_t)nch + (uint32_t)c;
+        const int st = (int)(i % ns);
+        while (tag[st] != i) {
+        }
+        mbar_wait(&full[st], (i / ns) & 1);
+        const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
+        const double2* saa = reinterpret_cast<const double2*>(stage);
+        const int32_t* sja = reinterpret_cast<const int32_t*>(stage + A.ja_off);
+#pragma unroll
+        for (int v = 0; v < NX; ++v) {
+            const double2* xv = v == 0 ? x0 : x1;
+            if (A.cm == 0) {
+                if (len > 0) acc[v].full_row(A, xv, saa, sja, lane);
+            } else {
+                const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
+                if (len > c0) acc[v].chunk(A, xv, saa, sja, lane, c, c0);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    RowVals<NX> out;
+#pragma unroll
+    for (int v = 0; v < NX; ++v) out.v[v] = acc[v].result();
+    return out;
+}
+
+// ---- fused reductions: consumer warps -> stash ring -> reducer warp --------
+// Per row the body returns NC complex and NR real reduction terms; the
+// consumer warp that owns a slice writes them into stash slot
+// (CTA slice sequence number) % kStashSlices and arrives on that slot's
+// `sfull` barrier.  The reducer warp takes the slices of each 4096-row block
+// in order, sums every pairwise leaf of the block's plans as soon as all its
+// rows are in (leaf_upto table), releases slots no pending leaf still needs
+// (`sfree`), and after the last leaf combines the tree, stores the block
+// partials and counts the arrival.  The reducer of the CTA retiring the last
+// block folds all partials in order (vecops.py:159-161) and hands the totals
+// to body.finish().  Consumers therefore never wait for a reduction.
+struct RedCfg {
+    PlanPtrs pc, pr;       // complex / real plans (vecops.py DEFAULT_PLAN, 4096)
+    double* partials;      // nblocks x (2 NC + NR) doubles
+    unsigned int* counter; // block arrivals (reset by body.finish)
+};
+
+constexpr int kPlanCache = 2560;  // bytes of shared memory per cached plan (full-block plans: ~2.0 / 1.3 KB)
+constexpr int kLeafBatchRows = 256;  // the reducer sums leaves in batches of about this many rows
+
+template <int NC, int NR>
+struct RedSmem {
+    static constexpr size_t kBars = 2 * kStashSlices * 8;
+    static constexpr size_t kStashC = (size_t)kStashSlices * kSlice * NC * 16;
+    static constexpr size_t kStashR = (size_t)kStashSlices * kSlice * NR * 8;
+    static constexpr size_t kNodesC = (size_t)kNodeSlots * NC * 16;
+    static constexpr size_t kNodesR = (size_t)kNodeSlots * NR * 8;
+    static constexpr size_t kPlans = (size_t)kPlanCache * ((NC > 0) + (NR > 0));
+    static constexpr size_t kBytes = (NC + NR) ? kBars + kStashC + kStashR + kNodesC + kNodesR + kPlans : 0;
+    unsigned char* base;
+    __device__ uint64_t* sfull() const { return reinterpret_cast<uint64_t*>(base); }
+    __device__ uint64_t* sfree() const { return reinterpret_cast<uint64_t*>(base) + kStashSlices; }
+    __device__ double2* stc() const { return reinterpret_cast<double2*>(base + kBars); }
+    __device__ double* str() const { return reinterpret_cast<double*>(base + kBars + kStashC); }
+    __device__ double2* ndc() const { return reinterpret_cast<double2*>(base + kBars + kStashC + kStashR); }
+    __device__ double* ndr() const { return reinterpret_cast<double*>(base + kBars + kStashC + kStashR + kNodesC); }
+    __device__ char* planc() const { return reinterpret_cast<char*>(base + kBars + kStashC + kStashR + kNodesC + kNodesR); }
+    __device__ char* planr() const { return planc() + (NC > 0 ? kPlanCache : 0); }
+};
+
+// Copies a plan blob into shared memory (whole warp); returns the pointer to
+// use (the global copy when it does not fit).
+__device__ __forceinline__ const char* cache_plan(const char* g, char* s) {
+    const PlanHeader* h = reinterpret_cast<const PlanHeader*>(g);
+    const int bytes = h->ops_off + 16 * h->nops;
+    if (bytes > kPlanCache) return g;
+    const int4* src = reinterpret_cast<const int4*>(g);
+    int4* dst = reinterpret_cast<int4*>(s);
+    for (int i = threadIdx.x & 31; i < (bytes + 15) / 16; i += 32) dst[i] = src[i];
+    __syncwarp();
+    return s;
+}
+
+// Leaves [lo, hi) of `plan` over the stash (segment element e = block row
+// 1 + e at stash row (rowbase + e) & kStashMask).  One (leaf, lane) item per
+// warp lane; the item's <= 16 elements are loaded before the in-order adds.
+template <typename V, int NACC>
+__device__ __forceinline__ void red_leaves(const char* plan, const V* stash, uint32_t rowbase, V* nodes, int lo,
+                                           int hi) {
+    constexpr int LANES = VT<V>::lanes;
+    constexpr int GMAX = (LANES == 4 ? 64 : 128) / LANES;  // 16
+    const PlanHeader* h = reinterpret_cast<const PlanHeader*>(plan);
+    const int lane = threadIdx.x & 31;
+    if (h->seq) {  // L < lanes: one sequential leaf from -0.0
+        if (lane == 0) {
+            V sacc[NACC];
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) sacc[a] = VT<V>::negzero();
+            for (int k = 0; k < h->L; ++k) {
+                const uint32_t r = (rowbase + (uint32_t)k) & kStashMask;
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) sacc[a] = VT<V>::add(sacc[a], stash[r * NACC + a]);
+            }
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) nodes[a] = sacc[a];
+        }
+        return;
+    }
+    const int2* leaves = reinterpret_cast<const int2*>(plan + h->leaves_off);
+    const int q = lane & (LANES - 1);
+    for (int it0 = lo * LANES; it0 < hi * LANES; it0 += 32) {
+        const int itm = it0 + lane;
+        const bool valid = itm < hi * LANES;
+        const int leaf = itm / LANES;
+        const int2 lf = valid ? leaves[leaf] : make_int2(0, 0);
+        const int G = lf.y / LANES;
+        const int rem = lf.y - G * LANES;
+        const uint32_t r0 = rowbase + (uint32_t)(lf.x + q);
+        V vals[GMAX][NACC];
+#pragma unroll
+        for (int g = 0; g < GMAX; ++g) {
+            if (g < G) {
+                const uint32_t r = (r0 + (uint32_t)(LANES * g)) & kStashMask;
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) vals[g][a] = stash[r * NACC + a];
+            }
+        }
+        V acc[NACC];
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) acc[a] = vals[0][a];
+#pragma unroll
+        for (int g = 1; g < GMAX; ++g) {
+            if (g < G) {
+#pragma unroll
+                for (int a = 0; a < NACC; ++a) acc[a] = VT<V>::add(acc[a], vals[g][a]);
+            }
+        }
+        // lane tree: (l0+l1)+(l2+l3) [+ ((l4+l5)+(l6+l7)) for real]
+#pragma unroll
+        for (int d = 1; d < LANES; d <<= 1) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) {
+                V o = VT<V>::shfl_down(acc[a], d);
+                if ((q & (2 * d - 1)) == 0) acc[a] = VT<V>::add(acc[a], o);
+            }
+        }
+        // leftovers (q < rem), added in order by the leaf's lane 0
+        V left[NACC];
+        const uint32_t rl = (r0 + (uint32_t)(LANES * G)) & kStashMask;
+#pragma unroll
+        for (int a = 0; a < NACC; ++a) left[a] = (valid && q < rem) ? stash[rl * NACC + a] : VT<V>::zero();
+        const int grp = lane & ~(LANES - 1);
+#pragma unroll
+        for (int j = 0; j < LANES - 1; ++j) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) {
+                V o = VT<V>::shfl(left[a], grp + j);
+                if (j < rem) acc[a] = VT<V>::add(acc[a], o);
+            }
+        }
+        if (valid && q == 0) {
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) nodes[leaf * NACC + a] = acc[a];
+        }
+    }
+}
+
+// Internal nodes in the plan's round order (one warp, __syncwarp per round).
+template <typename V, int NACC>
+__device__ __forceinline__ void red_tree(const char* plan, V* nodes, V (&pw)[NACC]) {
+    const PlanHeader* h = reinterpret_cast<const PlanHeader*>(plan);
+    const int lane = threadIdx.x & 31;
+    if (h->L <= 0) return;
+    __syncwarp();
+    if (!h->seq) {
+        const int4* ops = reinterpret_cast<const int4*>(plan + h->ops_off);
+        for (int r = 0; r < h->nrounds; ++r) {
+            const int lo = h->round_off[r], hi = h->round_off[r + 1];
+            for (int o = lo + lane; o < hi; o += 32) {
+                const int4 opn = ops[o];
+#pragma unroll
+                for (int a = 0; a < NACC; ++a)
+                    nodes[opn.x * NACC + a] = VT<V>::add(nodes[opn.y * NACC + a], nodes[opn.z * NACC + a]);
+            }
+            __syncwarp();
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NACC; ++a) pw[a] = nodes[h->root * NACC + a];
+}
+
+template <int NC, int NR, class Body>
+__device__ __noinline__ void reducer_warp(const SellView A, Body body, const RedCfg R, RedSmem<NC, NR> sm) {
+    constexpr int NP = 2 * NC + NR;
+    constexpr int kBatchC = kLeafBatchRows / 64, kBatchR = kLeafBatchRows / 128;
+    const int lane = threadIdx.x & 31;
+    const char* pc_full = NC ? cache_plan(R.pc.full, sm.planc()) : nullptr;
+    const char* pr_full = NR ? cache_plan(R.pr.full, sm.planr()) : nullptr;
+    uint32_t m = 0;  // CTA slice sequence number of the block's first slice
+    for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
+        const int64_t base = blk * kBlock;
+        const int64_t nrows = (A.n_rows - base < kBlock) ? A.n_rows - base : kBlock;
+        const int nsl = (int)((nrows + kSlice - 1) / kSlice);
+        const char* pcp = nullptr;
+        const char* prp = nullptr;
+        if (NC) pcp = nrows == kBlock ? pc_full : R.pc.tail;
+        if (NR) prp = nrows == kBlock ? pr_full : R.pr.tail;
+        const PlanHeader* hc = reinterpret_cast<const PlanHeader*>(pcp);
+        const PlanHeader* hr = reinterpret_cast<const PlanHeader*>(prp);
+        const int nlc = NC ? hc->nleaves : 0, nlr = NR ? hr->nleaves : 0;
+        const uint32_t rowbase = m * kSlice + 1;  // stash row of segment element 0 (block row 1)
+        int lc = 0, lr = 0, rel = 0;
+        double2 v0c[NC > 0 ? NC : 1];
+        double v0r[NR > 0 ? NR : 1];
+        for (int j = 0; j < nsl; ++j) {
+            const uint32_t sq = m + (uint32_t)j;
+            mbar_wait(&sm.sfull()[sq % kStashSlices], (sq / kStashSlices) & 1);
+            const bool lastj = j + 1 == nsl;
+            if (j == 0) {
+                const int k0 = (int)((m * kSlice) & kStashMask);
+#pragma unroll
+                for (int a = 0; a < NC; ++a) v0c[a] = sm.stc()[k0 * NC + a];
+#pragma unroll
+                for (int a = 0; a < NR; ++a) v0r[a] = sm.str()[k0 * NR + a];
+            }
+            int need = (int)nrows;  // first block row a pending leaf still reads
+            bool worked = false;
+#if defined(ZK_EXP) && ZK_EXP >= 1 && ZK_EXP < 10  // timing experiment: no leaf work (wrong results)
+            if (lane == 0) mbar_arrive(&sm.sfree()[sq % kStashSlices]);
+            rel = j + 1;
+            continue;
+#endif
+            if constexpr (NC > 0) {
+                const int hi = lastj ? nlc : min((int)hc->leaf_upto[j + 1], nlc);
+                if (hi - lc >= kBatchC || (lastj && hi > lc)) {
+                    red_leaves<double2, NC>(pcp, sm.stc(), rowbase, sm.ndc(), lc, hi);
+                    lc = hi;
+                    worked = true;
+                }
+                if (lc < nlc) need = min(need, 1 + reinterpret_cast<const int2*>(pcp + hc->leaves_off)[lc].x);
+            }
+            if constexpr (NR > 0) {
+                const int hi = lastj ? nlr : min((int)hr->leaf_upto[j + 1], nlr);
+                if (hi - lr >= kBatchR || (lastj && hi > lr)) {
+                    red_leaves<double, NR>(prp, sm.str(), rowbase, sm.ndr(), lr, hi);
+                    lr = hi;
+                    worked = true;
+                }
+                if (lr < nlr) need = min(need, 1 + reinterpret_cast<const int2*>(prp + hr->leaves_off)[lr].x);
+            }
+            const int upto = lastj ? nsl : min(j + 1, need / kSlice);
+            if (upto > rel) {
+                if (worked) __syncwarp();  // every lane is done reading the released rows
+                if (lane == 0)
+                    for (int k = rel; k < upto; ++k) mbar_arrive(&sm.sfree()[(m + (uint32_t)k) % kStashSlices]);
+                rel = upto;
+            }
+        }
+        m += (uint32_t)nsl;
+        double2 pwc[NC > 0 ? NC : 1];
+        double pwr[NR > 0 ? NR : 1];
+        if constexpr (NC > 0) red_tree<double2, NC>(pcp, sm.ndc(), pwc);
+        if constexpr (NR > 0) red_tree<double, NR>(prp, sm.ndr(), pwr);
+        unsigned int last = 0;
+        if (lane == 0) {
+            double* P = R.partials + blk * NP;
+#pragma unroll
+            for (int a = 0; a < NC; ++a) {
+                const double2 t = hc->L > 0 ? cadd(v0c[a], pwc[a]) : v0c[a];
+                P[2 * a] = t.x;
+                P[2 * a + 1] = t.y;
+            }
+#pragma unroll
+            for (int a = 0; a < NR; ++a) P[2 * NC + a] = hr->L > 0 ? __dadd_rn(v0r[a], pwr[a]) : v0r[a];
+            __threadfence();
+            last = (atomicAdd(R.counter, 1u) == (unsigned)A.nblocks - 1) ? 1u : 0u;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        __syncwarp();
+        if (last) {
+            __threadfence();
+            double tot[NP];
+            // the stash is free now (every slice of this CTA was reduced): fold scratch
+            warp_fold<double>(R.partials, NP, A.nblocks, reinterpret_cast<double*>(sm.stc()),
+                              (int)((RedSmem<NC, NR>::kStashC + RedSmem<NC, NR>::kStashR) / (8 * NP)), tot);
+            if (lane == 0) body.finish(tot);
+        }
     }
 }
 
 // Persistent pipelined SpMV over the CTA's 4096-row blocks (blk = blockIdx.x,
 // +gridDim.x, ...).  For each row the consumer thread calls
-// ctx = body.prefetch(row) before the row's products (so the epilogue
-// operands are in flight during the row computation), then
-// body.row(row, value, ctx).  Bodies with reductions (Body::kReduce) get
-// window_done(blk, slices) after every window of A.win slices and
-// block_done(blk) after the block's last row, each behind a named barrier
-// over the consumer warps; plain bodies never synchronise the consumers.
-// The producer warp exits once it has issued every chunk.  `smem` holds
-// kBarBytes + ns*stage_bytes bytes.
-template <bool SWAP, class Body>
-__device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* __restrict__ x, Body& body,
+// body.row(row, values, svals, tc, tr), which stores the row's outputs and
+// returns its Body::kNC complex / Body::kNR real reduction terms (see
+// reducer_warp; plain bodies have none, PipeWarps gives the warp roles).
+// svals are the row's entries of the Body::kSV vectors A.sv[] (the
+// epilogue's operands), which the producer stages with the slice by TMA, so
+// they cost the consumer neither registers nor load latency.  NX = 2 multiplies the matrix with two vectors in
+// one pass over it.  `smem` holds kBarBytes + ns*stage_bytes + RedSmem bytes.
+template <bool SWAP, int NX, class Body>
+__device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* __restrict__ x0,
+                                              const double2* __restrict__ x1, Body& body, const RedCfg& R,
                                               unsigned char* smem) {
+    constexpr int NC = Body::kNC, NR = Body::kNR;
+    constexpr bool kRed = (NC + NR) > 0;
+    constexpr int kCW = PipeWarps<kRed>::consumers;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);
     uint64_t* empty = full + kMaxStages;
     // tag[st] = CTA-local index of the chunk the producer last armed stage st
@@ -368,6 +846,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
     // written before the stage's arrive: visible after the full-barrier wait
     uint32_t* wid = reinterpret_cast<uint32_t*>(empty + kMaxStages) + kMaxStages;
     unsigned char* ring = smem + kBarBytes;
+    RedSmem<NC, NR> sm{ring + (size_t)A.ns * A.stage_bytes};
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ns = A.ns, nch = A.nch;
     const int cols = 1 + 4 * A.cm;
@@ -378,10 +857,22 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             mbar_init(&empty[i], 1);
             tag[i] = 0xffffffffu;
         }
+        if (kRed) {
+            for (int i = 0; i < kStashSlices; ++i) {
+                mbar_init(&sm.sfull()[i], 1);
+                mbar_init(&sm.sfree()[i], 1);
+            }
+        }
         mbar_fence_init();
     }
     __syncthreads();
-    if (warp == kConsumerWarps) {  // producer warp: lane l owns ring stage l
+    if constexpr (kRed) {
+        if (warp == PipeWarps<kRed>::reducer) {
+            reducer_warp<NC, NR>(A, body, R, sm);
+            return;
+        }
+    }
+    if (warp == PipeWarps<kRed>::producer) {  // producer warp: lane l owns ring stage l
         // Chunk i of the CTA's sequence uses stage i % ns, so lane l issues
         // chunks l, l + ns, l + 2ns, ... in order; each lane polls its own
         // empty barrier without blocking, so the lanes progress independently
@@ -392,6 +883,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
         int64_t off0 = 0, off1 = 0, s = 0;
         int c = 0, w = 0;
         bool active = false;
+        int32_t cm_hi = -1, cm_lo = 0;  // x columns to prefetch for chunk i
         auto locate = [&]() {  // coordinates + offsets of chunk i (loads issued early)
             const uint32_t seq = i / (uint32_t)nch;
             c = (int)(i % (uint32_t)nch);
@@ -401,6 +893,11 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             if (active) {
                 off0 = __ldg(A.slice_off + s);
                 off1 = __ldg(A.slice_off + s + 1);
+                // leading edge of the x window: columns above the previous
+                // slice's largest (a block's first slice: the 4096 below its own)
+                cm_hi = __ldg(A.slice_cmax + s);
+                cm_lo = (s % kSlicesPerBlock != 0) ? __ldg(A.slice_cmax + s - 1) + 1 : cm_hi - (kBlock - 1);
+                if (cm_lo < 0) cm_lo = 0;
             }
         };
         if (owner) locate();
@@ -409,15 +906,26 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
                 w = (int)((off1 - off0) / kSlice);
                 tag[lane] = i;
                 unsigned char* stage = ring + (size_t)lane * A.stage_bytes;
-                if (A.cm == 0) {  // whole slice + its row lengths
+                if (A.cm == 0) {  // whole slice + its row lengths + the staged vector rows
                     wid[lane] = (uint32_t)w;
                     const uint32_t cnt = (uint32_t)w * kSlice;
+                    const int64_t r0 = s * kSlice;
+                    const uint32_t vrows = (uint32_t)min((int64_t)kSlice, A.n_rows - r0);
+#if defined(ZK_EXP) && ZK_EXP >= 2 && ZK_EXP < 10
                     mbar_arrive_expect_tx(&full[lane], cnt * 20u + kSlice);
+#else
+                    mbar_arrive_expect_tx(&full[lane], cnt * 20u + kSlice + (uint32_t)A.nsv * vrows * 16u);
+#endif
                     if (cnt) {
                         bulk_g2s(stage, A.aa + off0, cnt * 16u, &full[lane], pol);
                         bulk_g2s(stage + A.ja_off, A.ja + off0, cnt * 4u, &full[lane], pol);
                     }
-                    bulk_g2s(stage + A.rl_off, A.rowlen + s * kSlice, kSlice, &full[lane], pol);
+                    bulk_g2s(stage + A.rl_off, A.rowlen + r0, kSlice, &full[lane], pol);
+#if defined(ZK_EXP) && ZK_EXP >= 2 && ZK_EXP < 10
+                    if (0)
+#endif
+                    for (int v = 0; v < A.nsv; ++v)
+                        bulk_g2s(stage + A.sv_off + v * kSlice * 16, A.sv[v] + r0, vrows * 16u, &full[lane], pol);
                 } else {
                     const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
                     const int c1 = min(w, cols + 4 * A.cm * c);
@@ -429,6 +937,11 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
                         bulk_g2s(stage + A.ja_off, A.ja + off, cnt * 4u, &full[lane], pol);
                     }
                 }
+                if (c == 0 && cm_hi >= cm_lo) {  // x rows this slice is first to touch -> L2
+                    const uint32_t nb = (uint32_t)min(cm_hi - cm_lo + 1, 4096) * 16u;
+                    bulk_prefetch_l2(x0 + cm_lo, nb);
+                    if (x1) bulk_prefetch_l2(x1 + cm_lo, nb);
+                }
                 i += (uint32_t)ns;
                 ++u;
                 locate();
@@ -436,95 +949,117 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
         }
         return;
     }
+    // ---- consumer warps: warp w takes slices w, w+kCW, ... of each block ----
     const bool fast = A.cm == 0 && A.fma;
+#if defined(ZK_EXP) && ZK_EXP >= 10
+    unsigned long long dbg_wait = 0, dbg_comp = 0, dbg_n = 0, dbg_uni = 0, dbg_iss = 0, dbg_lat = 0, dbg_rest = 0;
+#endif
     uint32_t sbase = 0;  // CTA-local index of the block's first slice
     for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
         const int64_t s_lo = blk * kSlicesPerBlock;
         const int64_t s_hi = (s_lo + kSlicesPerBlock < A.nslices) ? s_lo + kSlicesPerBlock : A.nslices;
         const int nsl = (int)(s_hi - s_lo);
-        // windows of A.win slices; after each (but the last) the body may
-        // reduce everything that lies entirely in the rows done so far
-        const int win = Body::kReduce ? A.win : nsl;
-        for (int w0 = 0; w0 < nsl; w0 += win) {
-        const int w1 = min(nsl, w0 + win);
-        for (int j = w0 + warp; j < w1; j += kConsumerWarps) {
+        for (int j = warp; j < nsl; j += kCW) {
             const int64_t row = (s_lo + j) * kSlice + lane;
+            const uint32_t sq = sbase + (uint32_t)j;  // CTA slice sequence number
+            const bool mine = row < A.n_rows;
+            constexpr int SV = Body::kSV;
+            double2 svals[SV > 0 ? SV : 1];  // the row's epilogue operands (staged with the slice)
+            RowVals<NX> val;
+            int len;
             if (fast) {
-                const uint32_t i = sbase + (uint32_t)j;
-                const uint32_t q = __umulhi(i, A.ns_magic);
-                const int st = (int)(i - q * (uint32_t)ns);
-                while (tag[st] != i) {
+#if defined(ZK_EXP) && ZK_EXP >= 10
+                const long long t0 = clock64();
+#endif
+                const uint32_t q = __umulhi(sq, A.ns_magic);
+                const int st = (int)(sq - q * (uint32_t)ns);
+                while (tag[st] != sq) {
                 }
                 mbar_wait(&full[st], q & 1);
+#if defined(ZK_EXP) && ZK_EXP >= 10
+                const long long t1 = clock64();
+#endif
                 const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
                 const int W = (int)wid[st];
-                const int len = stage[A.rl_off + lane];
-                const bool mine = row < A.n_rows && len != 255;
-                typename Body::RowCtx ctx;
-                if (mine) ctx = body.prefetch(row);
-                const double2 val = row_fast_dispatch<SWAP>(W, x, reinterpret_cast<const double2*>(stage),
-                                                            reinterpret_cast<const int32_t*>(stage + A.ja_off),
-                                                            lane, mine ? len : 0);
+                len = stage[A.rl_off + lane];
+                val = row_fast_dispatch<SWAP, NX>(W, x0, x1, reinterpret_cast<const double2*>(stage),
+                                                  reinterpret_cast<const int32_t*>(stage + A.ja_off), lane,
+                                                  (mine && len != 255) ? len : 0, !mine);
+#if defined(ZK_EXP) && ZK_EXP >= 2 && ZK_EXP < 10
+#pragma unroll
+                for (int v = 0; v < SV; ++v) svals[v] = A.sv[v][mine ? row : 0];
+#else
+#pragma unroll
+                for (int v = 0; v < SV; ++v)
+                    svals[v] = reinterpret_cast<const double2*>(stage + A.sv_off)[v * kSlice + lane];
+#endif
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
-                if (mine) body.row(row, val, ctx);
-                continue;
-            }
-            const int len = A.rowlen[row];
-            const bool mine = row < A.n_rows && len != 255;
-            typename Body::RowCtx ctx;
-            if (mine) ctx = body.prefetch(row);
-            RowAcc acc;
-            acc.init(mine ? len : 0);
-            for (int c = 0; c < nch; ++c) {
-                const uint32_t i = (sbase + (uint32_t)j) * (uint32_t)nch + (uint32_t)c;
-                const int st = (int)(i % ns);
-                while (tag[st] != i) {
+#if defined(ZK_EXP) && ZK_EXP >= 10
+                const long long t2 = clock64();
+                const bool uni = __all_sync(0xffffffffu, !mine || len == W);
+                dbg_wait += t1 - t0;
+                dbg_comp += t2 - t1;
+#if ZK_EXP >= 11
+                if (uni) {
+                    dbg_iss += zk_dbg_sh[warp * 2] - t1;
+                    dbg_lat += zk_dbg_sh[warp * 2 + 1] - zk_dbg_sh[warp * 2];
+                    dbg_rest += t2 - zk_dbg_sh[warp * 2 + 1];
                 }
-                mbar_wait(&full[st], (i / ns) & 1);
-                const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
-                if (A.cm == 0) {
-                    if (mine)
-                        acc.full_row(A, x, reinterpret_cast<const double2*>(stage),
-                                     reinterpret_cast<const int32_t*>(stage + A.ja_off), lane);
-                } else {
-                    const int c0 = c == 0 ? 0 : 1 + 4 * A.cm * c;
-                    if (mine && len > c0)
-                        acc.chunk(A, x, reinterpret_cast<const double2*>(stage),
-                                  reinterpret_cast<const int32_t*>(stage + A.ja_off), lane, c, c0);
+#endif
+                dbg_n += 1;
+                dbg_uni += uni ? 1 : 0;
+#endif
+            } else {
+                len = A.rowlen[row];
+                val = generic_slice<NX>(A, x0, x1, full, empty, tag, ring, sq, lane, (mine && len != 255) ? len : 0);
+#pragma unroll
+                for (int v = 0; v < SV; ++v) svals[v] = mine ? A.sv[v][row] : make_double2(0.0, 0.0);
+            }
+            if (mine && len == 255) {  // long row: side CSR, full pairwise recursion
+                const int li = long_index(A, blk, row);
+                val.v[0] = long_row_sum(A, x0, li);
+                if constexpr (NX == 2) val.v[1] = long_row_sum(A, x1, li);
+            }
+            double2 tc[NC > 0 ? NC : 1];
+            double tr[NR > 0 ? NR : 1];
+            if (mine) body.row(row, val.v, svals, tc, tr);
+            if (kRed) {
+                if (sq >= (uint32_t)kStashSlices) mbar_wait(&sm.sfree()[sq % kStashSlices], ((sq / kStashSlices) - 1) & 1);
+                const int k = (int)((sq * kSlice + lane) & kStashMask);
+                if (mine) {
+#pragma unroll
+                    for (int a = 0; a < NC; ++a) sm.stc()[k * NC + a] = tc[a];
+#pragma unroll
+                    for (int a = 0; a < NR; ++a) sm.str()[k * NR + a] = tr[a];
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[st]);
+                if (lane == 0) mbar_arrive(&sm.sfull()[sq % kStashSlices]);
             }
-            if (mine) body.row(row, acc.result(), ctx);
-        }
-        if (Body::kReduce && w1 < nsl) {
-            named_sync(1, kConsumers);
-            body.window_done(blk, w1);
-        }
         }
         sbase += (uint32_t)nsl;
-        if (A.long_blk_ptr) {
-            const int lb = A.long_blk_ptr[blk], le = A.long_blk_ptr[blk + 1];
-            for (int li = lb + (int)threadIdx.x; li < le; li += kConsumers) {
-                const int64_t row = (int64_t)A.long_row[li];
-                typename Body::RowCtx ctx = body.prefetch(row);
-                body.row(row, long_row_sum(A, x, li), ctx);
-            }
-        }
-        if (Body::kReduce) {
-            named_sync(1, kConsumers);
-            body.block_done(blk);
-        }
     }
+#if defined(ZK_EXP) && ZK_EXP >= 10
+    if (lane == 0) {
+        atomicAdd(&zk_dbg[0], dbg_wait);
+        atomicAdd(&zk_dbg[1], dbg_comp);
+        atomicAdd(&zk_dbg[2], dbg_n);
+        atomicAdd(&zk_dbg[6], dbg_uni);
+        atomicAdd(&zk_dbg[5], dbg_n - dbg_uni);
+        atomicAdd(&zk_dbg[7], dbg_iss);
+        atomicAdd(&zk_dbg[8], dbg_lat);
+        atomicAdd(&zk_dbg[9], dbg_rest);
+    }
+#endif
 }
 
 // Kernel-side dispatch on numpy's elision swap (a launch-uniform flag).
-template <class Body>
-__device__ __forceinline__ void sell_run(const SellView& A, const double2* __restrict__ x, Body& body,
+template <int NX, class Body>
+__device__ __forceinline__ void sell_run(const SellView& A, const double2* __restrict__ x0,
+                                         const double2* __restrict__ x1, Body& body, const RedCfg& R,
                                          unsigned char* smem) {
-    if (A.swap) sell_pipeline<true>(A, x, body, smem);
-    else sell_pipeline<false>(A, x, body, smem);
+    if (A.swap) sell_pipeline<true, NX>(A, x0, x1, body, R, smem);
+    else sell_pipeline<false, NX>(A, x0, x1, body, R, smem);
 }
 
 }  // namespace zk
