@@ -157,6 +157,59 @@ zk_status zk_bicgstab(zk_context* ctx, const zk_csr* A, const double* b, const d
                       const double* x0, double tolerance, int64_t max_iterations, double* x_out,
                       double* history_host, zk_solve_report* report);
 
+/* ---- row-sharded BiCGStab (multi-GPU) --------------------------
+ * One shard per rank (process / GPU).  The reference has no distributed
+ * solver: a shard runs exactly the loop of krylov.solve_bicgstab
+ * (krylov.py:213-295) on its rows and the ranks combine every reduction in
+ * the unsharded block order, so all ranks -- and the 1-GPU solve and the
+ * reference -- produce the same bits.  The library does the device work;
+ * the caller's transport (NCCL or host staging, paper_2112_06465_b200/dist.py)
+ * moves halos and block partials between the phases:
+ *   - A_local: rows [row0, row0 + n) of the matrix, row0 a multiple of 4096
+ *     (the reduction block), columns renumbered own rows first ([0, n)) and
+ *     the n_halo external columns after, in ascending global order;
+ *   - before SETUP / TRUE_RES_S / TRUE_RES the halo of ZK_DVEC_X, before
+ *     PIVOT that of ZK_DVEC_PHAT, before SPMV_T that of ZK_DVEC_SHAT must be
+ *     current (zk_dshard_pack gathers the entries a peer needs);
+ *   - after every phase with a reduction, each rank's ZK_DVEC_PARTIALS
+ *     (max_blocks * 4 doubles) is all-gathered into ZK_DVEC_GATHERED (rank r
+ *     at r * max_blocks * 4) and zk_dshard_finish folds it.
+ * Phases whose work depends on the s-check (X_ALPHA, TRUE_RES_S) are no-ops
+ * on the device when it did not fire, so every rank issues the same calls. */
+typedef struct zk_dshard zk_dshard;
+#define ZK_DVEC_X 0
+#define ZK_DVEC_PHAT 1
+#define ZK_DVEC_SHAT 2
+#define ZK_DVEC_B 3
+#define ZK_DVEC_MINV 4
+#define ZK_DVEC_PARTIALS 5
+#define ZK_DVEC_GATHERED 6
+#define ZK_DPHASE_SETUP 0       /* r0 = b - A x0, ||b||, ||r0||, <r0,r0>  (krylov.py:159-168) */
+#define ZK_DPHASE_P_FIRST 1     /* p = r (first iteration)                  (krylov.py:263-266) */
+#define ZK_DPHASE_PIVOT 2       /* v = A p^, <r~,v> -> alpha                (krylov.py:267-271) */
+#define ZK_DPHASE_S_UPDATE 3    /* s, s^, ||s|| -> s-check                  (krylov.py:272-275) */
+#define ZK_DPHASE_X_ALPHA 4     /* x += alpha p^ (s-check path)             (krylov.py:274) */
+#define ZK_DPHASE_TRUE_RES_S 5  /* ||b - A x|| on the s-check path          (krylov.py:276-279) */
+#define ZK_DPHASE_SPMV_T 6      /* t = A s^, <t,t>, <t,s> -> omega           (krylov.py:281-287) */
+#define ZK_DPHASE_XR_UPDATE 7   /* x, r updates, <r~,r> -> rho, beta         (krylov.py:288-290, 255-261) */
+#define ZK_DPHASE_TRUE_RES 8    /* ||b - A x|| -> record / stop              (krylov.py:291-294) */
+#define ZK_DPHASE_P_NEXT 9      /* p, p^ for the next iteration             (krylov.py:263-266) */
+zk_status zk_dshard_create(zk_context* ctx, zk_csr* A_local, int64_t n_halo, int64_t nnz_global, int jacobi,
+                           int64_t max_iterations, int nranks, int64_t max_blocks, zk_dshard** out);
+zk_status zk_dshard_destroy(zk_dshard* shard);
+/* Device pointer + length (complex entries; doubles for PARTIALS/GATHERED). */
+zk_status zk_dshard_vector(zk_dshard* shard, int which, double** dptr, int64_t* length);
+/* Start a solve (b, minv, and x0 when has_x0 already copied into the shard's vectors). */
+zk_status zk_dshard_reset(zk_dshard* shard, double tolerance, int64_t max_iterations, int has_x0);
+zk_status zk_dshard_phase(zk_dshard* shard, int phase);
+/* rank_blocks_host[r]: reduction blocks of rank r (its partials count). */
+zk_status zk_dshard_finish(zk_dshard* shard, int phase, const int64_t* rank_blocks_host);
+/* out[i] = vec[idx[i]] (device arrays): the entries a peer's halo needs. */
+zk_status zk_dshard_pack(zk_dshard* shard, int which, const int64_t* idx, int64_t count, double* out);
+/* Synchronises; done = 1 stopped (converged / cap / breakdown), 2 zero rhs. */
+zk_status zk_dshard_status(zk_dshard* shard, zk_solve_report* report, int32_t* done);
+zk_status zk_dshard_history(zk_dshard* shard, double* history_host, int64_t count);
+
 #ifdef __cplusplus
 }
 #endif

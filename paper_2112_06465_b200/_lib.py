@@ -95,6 +95,15 @@ SIGNATURES = {
     "zk_csr_bytes": [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "zk_spmv": [_vp, _vp, _vp, _vp],
     "zk_bicgstab": [_vp, _vp, _vp, _vp, _vp, _d, _i64, _vp, ctypes.POINTER(_d), ctypes.POINTER(SolveReportC)],
+    "zk_dshard_create": [_vp, _vp, _i64, _i64, _i, _i64, _i, _i64, ctypes.POINTER(_vp)],
+    "zk_dshard_destroy": [_vp],
+    "zk_dshard_vector": [_vp, _i, ctypes.POINTER(ctypes.POINTER(_d)), ctypes.POINTER(_i64)],
+    "zk_dshard_reset": [_vp, _d, _i64, _i],
+    "zk_dshard_phase": [_vp, _i],
+    "zk_dshard_finish": [_vp, _i, _vp],
+    "zk_dshard_pack": [_vp, _i, _vp, _i64, _vp],
+    "zk_dshard_status": [_vp, ctypes.POINTER(SolveReportC), ctypes.POINTER(ctypes.c_int32)],
+    "zk_dshard_history": [_vp, _vp, _i64],
 }
 STRING_FUNCS = ("zk_last_error", "zk_version")
 

@@ -102,6 +102,17 @@ void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, in
 zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
                    const int64_t* ia_d, const int64_t* ja_d, const double2* aa_d);
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y);
+struct DistSolver;
+DistSolver* dist_create(zk_context* c, zk_csr* A, int64_t n_halo, int64_t nnz_global, bool jacobi, int64_t maxit,
+                        int nranks, int64_t maxb);
+void dist_destroy(DistSolver* D);
+void* dist_vector(DistSolver* D, int which, int64_t* len);
+void dist_reset(DistSolver* D, double tol, int64_t maxit, bool has_x0);
+void dist_phase(DistSolver* D, int phase);
+void dist_finish(DistSolver* D, int phase, const int64_t* rank_blocks);
+void dist_pack(DistSolver* D, int which, const int64_t* idx, int64_t count, double2* out);
+void dist_status(DistSolver* D, zk_solve_report* rep, int32_t* done);
+void dist_history(DistSolver* D, double* host, int64_t count);
 int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
                     int64_t maxit, double2* x_out, double* history_host, zk_solve_report* rep);
 void destroy_solver_plan(zk_context* c, SolverPlan* P);
@@ -579,6 +590,89 @@ zk_status zk_bicgstab(zk_context* c, const zk_csr* A, const double* b, const dou
     if (st != ZK_OK) return st;
     if (rc == ZK_ERR_BREAKDOWN) set_error("breakdown");
     return rc;
+}
+
+// ---- row-sharded BiCGStab ----------------------------------------------------
+struct zk_dshard {
+    zk_context* ctx;
+    zk::DistSolver* d;
+};
+
+zk_status zk_dshard_create(zk_context* c, zk_csr* A, int64_t n_halo, int64_t nnz_global, int jacobi, int64_t maxit,
+                           int nranks, int64_t maxb, zk_dshard** out) {
+    return guarded([&] {
+        need_ctx(c);
+        need(A != nullptr && out != nullptr, ZK_ERR_PARAMETER, "null matrix/output");
+        need(n_halo >= 0 && A->n_cols == A->n_rows + n_halo, ZK_ERR_DIMENSION,
+             "shard columns must be its rows plus the halo");
+        need(A->n_rows > 0, ZK_ERR_DIMENSION, "empty shard");
+        need(maxit >= 1, ZK_ERR_PARAMETER, "max_iterations must be >= 1");
+        need(nranks >= 1 && nranks <= 64, ZK_ERR_PARAMETER, "1..64 ranks");
+        need(maxb >= (A->n_rows + 4095) / 4096, ZK_ERR_PARAMETER, "max_blocks below this shard's block count");
+        need(nnz_global >= A->nnz, ZK_ERR_PARAMETER, "global nnz below the shard's");
+        zk_dshard* h = new zk_dshard{c, zk::dist_create(c, A, n_halo, nnz_global, jacobi != 0, maxit, nranks, maxb)};
+        *out = h;
+    });
+}
+
+zk_status zk_dshard_destroy(zk_dshard* h) {
+    return guarded([&] {
+        if (!h) return;
+        zk::dist_destroy(h->d);
+        delete h;
+    });
+}
+
+zk_status zk_dshard_vector(zk_dshard* h, int which, double** dptr, int64_t* len) {
+    return guarded([&] {
+        need(h && dptr && len, ZK_ERR_PARAMETER, "null argument");
+        *dptr = static_cast<double*>(zk::dist_vector(h->d, which, len));
+    });
+}
+
+zk_status zk_dshard_reset(zk_dshard* h, double tol, int64_t maxit, int has_x0) {
+    return guarded([&] {
+        need(h != nullptr, ZK_ERR_PARAMETER, "null shard");
+        need(tol > 0, ZK_ERR_PARAMETER, "tolerance must be positive");
+        need(maxit >= 1, ZK_ERR_PARAMETER, "max_iterations must be >= 1");
+        zk::dist_reset(h->d, tol, maxit, has_x0 != 0);
+    });
+}
+
+zk_status zk_dshard_phase(zk_dshard* h, int phase) {
+    return guarded([&] {
+        need(h != nullptr, ZK_ERR_PARAMETER, "null shard");
+        zk::dist_phase(h->d, phase);
+    });
+}
+
+zk_status zk_dshard_finish(zk_dshard* h, int phase, const int64_t* rank_blocks) {
+    return guarded([&] {
+        need(h != nullptr && rank_blocks != nullptr, ZK_ERR_PARAMETER, "null argument");
+        zk::dist_finish(h->d, phase, rank_blocks);
+    });
+}
+
+zk_status zk_dshard_pack(zk_dshard* h, int which, const int64_t* idx, int64_t count, double* out) {
+    return guarded([&] {
+        need(h != nullptr, ZK_ERR_PARAMETER, "null shard");
+        need(count >= 0, ZK_ERR_DIMENSION, "negative count");
+        zk::dist_pack(h->d, which, idx, count, D2(out));
+    });
+}
+
+zk_status zk_dshard_status(zk_dshard* h, zk_solve_report* rep, int32_t* done) {
+    return guarded([&] {
+        need(h && rep && done, ZK_ERR_PARAMETER, "null argument");
+        zk::dist_status(h->d, rep, done);
+    });
+}
+
+zk_status zk_dshard_history(zk_dshard* h, double* host, int64_t count) {
+    return guarded([&] {
+        need(h && host, ZK_ERR_PARAMETER, "null argument");
+        zk::dist_history(h->d, host, count);
+    });
 }
 
 }  // extern "C"

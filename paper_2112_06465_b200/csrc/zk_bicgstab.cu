@@ -55,6 +55,7 @@ struct SolverBufs {
     SolverState* st;
     int64_t n, nblocks;
     bool jacobi, fma;
+    int dist;          // row-sharded solve: block partials are folded across ranks (k_dist_finish)
 };
 
 constexpr int kNodesPerBuf = 2 * 136;             // node slots per buffer (<= 129 nodes x NACC 2)
@@ -92,6 +93,7 @@ __device__ __forceinline__ void stop(SolverState* st, int32_t status, int32_t wh
 // ---- setup: r0 = b - A x0, ||b||, ||r0||, <r0, r0> (krylov.py:159-168, 255) ----
 struct SetupBody {
     static constexpr int kNC = 1, kNR = 2, kSV = 1;  // staged: b
+    static constexpr int kNP = 2 * kNC + kNR;
     SolverBufs B;
     __device__ void row(int64_t row, const double2 (&ax)[1], const double2 (&sv)[1], double2 (&tc)[1], double (&tr)[2]) {
         const double2 b = sv[0];
@@ -185,6 +187,7 @@ __device__ __forceinline__ void pivot_to_alpha(SolverState* st, double2 pivot) {
 // prologue instance, use_cond = 0, runs the first iteration's K2).
 struct PivotBody {
     static constexpr int kNC = 1, kNR = 0, kSV = 1;  // staged: r~
+    static constexpr int kNP = 2 * kNC + kNR;
     SolverBufs B;
     cudaGraphConditionalHandle cond;
     int use_cond;
@@ -214,6 +217,7 @@ __global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_pivot(SellView A, S
 // ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
 struct TBody {
     static constexpr int kNC = 2, kNR = 0, kSV = 1;  // staged: s
+    static constexpr int kNP = 2 * kNC + kNR;
     SolverBufs B;
     __device__ void row(int64_t row, const double2 (&at)[1], const double2 (&sv)[1], double2 (&tc)[2], double (&)[1]) {
         B.t[row] = at[0];
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_t(SellView A, Solve
 template <int MODE>
 struct ResBody {
     static constexpr int kNC = 0, kNR = 1, kSV = 1;  // staged: b
+    static constexpr int kNP = 2 * kNC + kNR;
     SolverBufs B;
     __device__ void row(int64_t, const double2 (&ax)[1], const double2 (&sv)[1], double2 (&)[1], double (&tr)[1]) {
         tr[0] = abs2_np(cadd(sv[0], f1(make_double2(-1.0, 0.0), ax[0], B.fma)));
@@ -344,6 +349,17 @@ struct SUpdateOp {
     }
 };
 
+// s-check decision from the folded ||s||^2 (krylov.py:275)
+struct SUpdFinish {
+    static constexpr int kNP = 1;
+    SolverBufs B;
+    __device__ void finish(const double* t) {
+        SolverState* st = B.st;
+        st->counter = 0;
+        st->scheck = (__ddiv_rn(__dsqrt_rn(t[0]), st->b_norm) <= st->tol) ? 1 : 0;
+    }
+};
+
 __global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
@@ -352,11 +368,13 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanP
     SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
     double* nodes = reinterpret_cast<double*>(smem + kFoldScratch);
     auto done = [&]() {
+        if (B.dist) {
+            if ((threadIdx.x & 31) == 0) st->counter = 0;
+            return;
+        }
         double ss;
         warp_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), kFoldScratch / 8, &ss);
-        if ((threadIdx.x & 31) != 0) return;
-        st->counter = 0;
-        st->scheck = (__ddiv_rn(__dsqrt_rn(ss), st->b_norm) <= st->tol) ? 1 : 0;
+        if ((threadIdx.x & 31) == 0) SUpdFinish{B}.finish(&ss);
     };
     persistent_blocks<double, 1>(pr, B.n, B.nblocks, op, nodes, B.partials, &st->counter, done);
 }
@@ -406,6 +424,23 @@ struct XrOp {
     }
 };
 
+// rho' = <r~, r> -> rho, beta of the next iteration (krylov.py:255-261)
+struct XrFinish {
+    static constexpr int kNP = 2;
+    SolverBufs B;
+    __device__ void finish(const double* t) {
+        SolverState* st = B.st;
+        st->counter = 0;
+        const double2 rho_next = make_double2(t[0], t[1]);
+        const double2 rho = st->rho, a = st->alpha, w = st->omega;
+        st->rho_old = rho;
+        st->rho = rho_next;
+        // beta for the next iteration (speculative: K61 stops before it is
+        // used if the loop ends, and breaks down on krylov.py:256-259's checks)
+        if (!small_py(rho) && !small_py(w)) st->beta = cmul_py(cdiv_py(rho_next, rho), cdiv_py(a, w));
+    }
+};
+
 __global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, PlanPtrs pc) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
@@ -415,18 +450,45 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, Plan
     double2* nodes = reinterpret_cast<double2*>(smem + kFoldScratch);
     double2* PC = reinterpret_cast<double2*>(B.partials);
     auto done = [&]() {
+        if (B.dist) {
+            if ((threadIdx.x & 31) == 0) st->counter = 0;
+            return;
+        }
         double2 rho_next;
         warp_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), kFoldScratch / 16, &rho_next);
-        if ((threadIdx.x & 31) != 0) return;
-        st->counter = 0;
-        const double2 rho = st->rho;
-        st->rho_old = rho;
-        st->rho = rho_next;
-        // beta for the next iteration (speculative: K61 stops before it is
-        // used if the loop ends, and breaks down on krylov.py:256-259's checks)
-        if (!small_py(rho) && !small_py(w)) st->beta = cmul_py(cdiv_py(rho_next, rho), cdiv_py(a, w));
+        if ((threadIdx.x & 31) == 0) XrFinish{B}.finish(reinterpret_cast<const double*>(&rho_next));
     };
     persistent_blocks<double2, 1>(pc, B.n, B.nblocks, op, nodes, PC, &st->counter, done);
+}
+
+// ---- row-sharded solve: cross-rank fold of the block partials -----------------
+// `gathered` holds every rank's block partials (rank r at r*maxb*NP, its
+// counts[r] blocks first), i.e. the global block order of the unsharded
+// vector (rank row ranges are 4096-aligned), so one warp folding them in
+// that order reproduces vecops.py:159-161 exactly, on every rank.
+constexpr int kMaxRanks = 64;
+struct RankCounts {
+    int64_t n[kMaxRanks];
+};
+
+template <class Fin>
+__global__ void __launch_bounds__(32) k_dist_finish(Fin fin, const double* __restrict__ gathered, int nranks,
+                                                    int64_t maxb, RankCounts counts, int phase_gate) {
+    __shared__ double scratch[4 * 512];
+    const SolverState* st = fin.B.st;
+    if (st->done || (phase_gate == 1 && !st->scheck)) return;
+    constexpr int NP = Fin::kNP;
+    double tot = 0.0;
+    bool first = true;
+    for (int r = 0; r < nranks; ++r) {
+        if (counts.n[r] <= 0) continue;
+        warp_fold_cont(gathered + (int64_t)r * maxb * NP, NP, counts.n[r], scratch, 512, tot, first);
+        first = false;
+    }
+    double t[NP];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) t[c] = __shfl_sync(0xffffffffu, tot, c);
+    if (threadIdx.x == 0) fin.finish(t);
 }
 
 }  // namespace
@@ -609,6 +671,41 @@ static SolverPlan* get_plan(zk_context* c, zk_csr* A, bool jacobi, int64_t maxit
     return P;
 }
 
+// Kernel geometry of every solver phase for matrix A and plan P (and the
+// kernels' shared-memory attributes).
+static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
+    SolverBufs& B = P->bufs;
+    const int64_t n = A->n_rows;
+    Launch L;
+    L.c = c;
+    L.P = P;
+    const size_t ex_s = RedSmem<1, 2>::kBytes, ex_p = RedSmem<1, 0>::kBytes, ex_t = RedSmem<2, 0>::kBytes,
+                 ex_r = RedSmem<0, 1>::kBytes;
+    L.As = sell_view(A, c, ex_s, 1);
+    L.As.sv[0] = B.b;
+    L.Ap = sell_view(A, c, ex_p, 1);
+    L.Ap.sv[0] = B.rs;
+    L.At = sell_view(A, c, ex_t, 1);
+    L.At.sv[0] = B.s;
+    L.Ar = sell_view(A, c, ex_r, 1);
+    L.Ar.sv[0] = B.b;
+    L.smem_s = pipe_smem_bytes(L.As, ex_s);
+    L.smem_p = pipe_smem_bytes(L.Ap, ex_p);
+    L.smem_t = pipe_smem_bytes(L.At, ex_t);
+    L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
+    L.pc = c->plans_for(n, kBlock, kComplex);
+    L.pr = c->plans_for(n, kBlock, kReal);
+    L.red = RedCfg{L.pc, L.pr, B.partials, &B.st->counter, B.dist};
+    L.nb = (unsigned)B.nblocks;
+    L.pg = pipe_grid(A);
+    L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
+    int64_t ewg = (n + 255) / 256;
+    int64_t cap = (int64_t)num_sms() * 8;
+    L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
+    set_attrs(L);
+    return L;
+}
+
 // Runs the solve; x_out/history_host/report filled.  Returns ZK_OK or
 // ZK_ERR_BREAKDOWN.
 int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
@@ -638,34 +735,7 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     h.maxit = maxit;
     ZK_CUDA(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
 
-    Launch L;
-    L.c = c;
-    L.P = P;
-    const size_t ex_s = RedSmem<1, 2>::kBytes, ex_p = RedSmem<1, 0>::kBytes, ex_t = RedSmem<2, 0>::kBytes,
-                 ex_r = RedSmem<0, 1>::kBytes;
-    L.As = sell_view(A, c, ex_s, 1);
-    L.As.sv[0] = B.b;
-    L.Ap = sell_view(A, c, ex_p, 1);
-    L.Ap.sv[0] = B.rs;
-    L.At = sell_view(A, c, ex_t, 1);
-    L.At.sv[0] = B.s;
-    L.Ar = sell_view(A, c, ex_r, 1);
-    L.Ar.sv[0] = B.b;
-    L.smem_s = pipe_smem_bytes(L.As, ex_s);
-    L.smem_p = pipe_smem_bytes(L.Ap, ex_p);
-    L.smem_t = pipe_smem_bytes(L.At, ex_t);
-    L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
-    L.pc = c->plans_for(n, kBlock, kComplex);
-    L.pr = c->plans_for(n, kBlock, kReal);
-    unsigned int* ctr = &B.st->counter;
-    L.red = RedCfg{L.pc, L.pr, B.partials, ctr};
-    L.nb = (unsigned)B.nblocks;
-    L.pg = pipe_grid(A);
-    L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
-    int64_t ewg = (n + 255) / 256;
-    int64_t cap = (int64_t)num_sms() * 8;
-    L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
-    set_attrs(L);
+    Launch L = make_launch(c, A, P);
     SolverState out;
     if (use_graph() && !c->profile) {
         if (!P->graph_ok) build_graph(L);
@@ -704,6 +774,183 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     rep->history_len = it + 1;
     rep->kernel_launches = kPrologueKernels + kBodyKernels * out.trips;
     return out.status == ST_BREAKDOWN ? ZK_ERR_BREAKDOWN : ZK_OK;
+}
+
+// ---- row-sharded BiCGStab: one shard per rank ---------------------
+// The local matrix holds rows [row0, row0 + n) with columns renumbered own
+// rows first ([0, n)) and halo columns after ([n, n + n_halo), ascending
+// global order); the vectors an SpMV gathers (x, p^, s^) carry the halo
+// region, which the caller's transport fills before each SpMV phase.  Every
+// reduction phase leaves its block partials in `partials` (dist = 1); the
+// caller all-gathers them (rank r's maxb*NP doubles at r*maxb*NP) and
+// dist_finish folds them in global block order and runs the scalar
+// recurrences, identically on every rank.
+struct DistSolver {  // behind zk_dshard
+    zk_context* c = nullptr;
+    zk_csr* A = nullptr;
+    SolverPlan* P = nullptr;
+    Launch L{};
+    int64_t n = 0, n_ext = 0, maxb = 0;
+    int nranks = 0;
+    double* gathered = nullptr;
+};
+
+DistSolver* dist_create(zk_context* c, zk_csr* A, int64_t n_halo, int64_t nnz_global, bool jacobi, int64_t maxit,
+                        int nranks, int64_t maxb) {
+    DistSolver* D = new DistSolver();
+    D->c = c;
+    D->A = A;
+    D->n = A->n_rows;
+    D->n_ext = A->n_rows + n_halo;
+    D->nranks = nranks;
+    D->maxb = maxb;
+    A->nnz_elide = nnz_global;  // numpy's elision decision is the unsharded matrix's
+    SolverPlan* P = new SolverPlan();
+    P->n = D->n;
+    P->jacobi = jacobi;
+    P->hist_cap = maxit + 1 > 1024 ? maxit + 1 : 1024;
+    SolverBufs& B = P->bufs;
+    const size_t vb = sizeof(double2) * (size_t)(D->n_ext ? D->n_ext : 1);
+    auto vec = [&]() {
+        double2* v = static_cast<double2*>(c->alloc.alloc(vb));
+        ZK_CUDA(cudaMemsetAsync(v, 0, vb, c->stream));
+        return v;
+    };
+    B.n = D->n;
+    B.nblocks = (D->n + kBlock - 1) / kBlock;
+    B.jacobi = jacobi;
+    B.fma = c->fma != 0;
+    B.dist = 1;
+    B.x = vec(); B.b = vec(); B.r = vec(); B.rs = vec(); B.p = vec(); B.v = vec(); B.s = vec(); B.t = vec();
+    B.minv = jacobi ? vec() : nullptr;
+    B.ph = jacobi ? vec() : B.p;
+    B.sh = jacobi ? vec() : B.s;
+    const int64_t pb = maxb > B.nblocks ? maxb : B.nblocks;
+    B.partials = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)(pb ? pb : 1)));
+    ZK_CUDA(cudaMemsetAsync(B.partials, 0, sizeof(double) * 4 * (size_t)(pb ? pb : 1), c->stream));
+    B.hist = static_cast<double*>(c->alloc.alloc(sizeof(double) * P->hist_cap));
+    B.st = static_cast<SolverState*>(c->alloc.alloc(sizeof(SolverState)));
+    D->gathered = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)nranks * (size_t)(maxb ? maxb : 1)));
+    D->P = P;
+    D->L = make_launch(c, A, P);
+    return D;
+}
+
+void dist_destroy(DistSolver* D) {
+    if (!D) return;
+    D->c->alloc.free(D->gathered);
+    destroy_solver_plan(D->c, D->P);
+    delete D;
+}
+
+void* dist_vector(DistSolver* D, int which, int64_t* len) {
+    SolverBufs& B = D->P->bufs;
+    switch (which) {
+        case ZK_DVEC_X: *len = D->n_ext; return B.x;
+        case ZK_DVEC_PHAT: *len = D->n_ext; return B.ph;
+        case ZK_DVEC_SHAT: *len = D->n_ext; return B.sh;
+        case ZK_DVEC_B: *len = D->n; return B.b;
+        case ZK_DVEC_MINV: *len = B.jacobi ? D->n : 0; return B.minv;
+        case ZK_DVEC_PARTIALS: *len = 4 * (D->maxb > B.nblocks ? D->maxb : B.nblocks); return B.partials;
+        case ZK_DVEC_GATHERED: *len = 4 * (int64_t)D->nranks * D->maxb; return D->gathered;
+        default: throw ZkError{ZK_ERR_PARAMETER, "unknown shard vector"};
+    }
+}
+
+void dist_reset(DistSolver* D, double tol, int64_t maxit, bool has_x0) {
+    SolverBufs& B = D->P->bufs;
+    if (maxit + 1 > D->P->hist_cap) throw ZkError{ZK_ERR_PARAMETER, "max_iterations above the shard's capacity"};
+    cudaStream_t s = D->c->stream;
+    const size_t vb = sizeof(double2) * (size_t)D->n_ext;
+    if (!has_x0) ZK_CUDA(cudaMemsetAsync(B.x, 0, vb, s));
+    ZK_CUDA(cudaMemsetAsync(B.p, 0, vb, s));
+    ZK_CUDA(cudaMemsetAsync(B.v, 0, vb, s));
+    SolverState h;
+    std::memset(&h, 0, sizeof(h));
+    h.tol = tol;
+    h.maxit = maxit;
+    ZK_CUDA(cudaMemcpyAsync(B.st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+}
+
+void dist_phase(DistSolver* D, int phase) {
+    const Launch& L = D->L;
+    cudaStream_t s = D->c->stream;
+    SolverBufs& B = D->P->bufs;
+    if (D->n == 0) throw ZkError{ZK_ERR_DIMENSION, "empty shard"};
+    switch (phase) {
+        case ZK_DPHASE_SETUP: k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); break;
+        case ZK_DPHASE_P_FIRST: k_p_first<<<L.ew, 256, 0, s>>>(B); break;
+        case ZK_DPHASE_PIVOT: k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, B, L.red, 0, 0); break;
+        case ZK_DPHASE_S_UPDATE: k_s_update<<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pr); break;
+        case ZK_DPHASE_X_ALPHA: k_x_alpha<<<L.ew, 256, 0, s>>>(B); break;
+        case ZK_DPHASE_TRUE_RES_S: k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
+        case ZK_DPHASE_SPMV_T: k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, B, L.red); break;
+        case ZK_DPHASE_XR_UPDATE: k_xr_update<<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pc); break;
+        case ZK_DPHASE_TRUE_RES: k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
+        case ZK_DPHASE_P_NEXT: k_p_next<<<L.ew, 256, 0, s>>>(B); break;
+        default: throw ZkError{ZK_ERR_PARAMETER, "unknown solver phase"};
+    }
+    ZK_CUDA(cudaGetLastError());
+    D->c->launches++;
+}
+
+void dist_finish(DistSolver* D, int phase, const int64_t* rank_blocks) {
+    if (D->nranks > kMaxRanks) throw ZkError{ZK_ERR_PARAMETER, "too many ranks"};
+    RankCounts rc{};
+    for (int r = 0; r < D->nranks; ++r) rc.n[r] = rank_blocks[r];
+    SolverBufs& B = D->P->bufs;
+    cudaStream_t s = D->c->stream;
+    const double* g = D->gathered;
+    const int nr = D->nranks;
+    const int64_t mb = D->maxb;
+    switch (phase) {
+        case ZK_DPHASE_SETUP: k_dist_finish<<<1, 32, 0, s>>>(SetupBody{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_PIVOT: k_dist_finish<<<1, 32, 0, s>>>(PivotBody{B, 0, 0}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_S_UPDATE: k_dist_finish<<<1, 32, 0, s>>>(SUpdFinish{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_TRUE_RES_S: k_dist_finish<<<1, 32, 0, s>>>(ResBody<0>{B}, g, nr, mb, rc, 1); break;
+        case ZK_DPHASE_SPMV_T: k_dist_finish<<<1, 32, 0, s>>>(TBody{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_XR_UPDATE: k_dist_finish<<<1, 32, 0, s>>>(XrFinish{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_TRUE_RES: k_dist_finish<<<1, 32, 0, s>>>(ResBody<1>{B}, g, nr, mb, rc, 0); break;
+        default: throw ZkError{ZK_ERR_PARAMETER, "phase has no reduction"};
+    }
+    ZK_CUDA(cudaGetLastError());
+    D->c->launches++;
+}
+
+__global__ void k_pack(const double2* __restrict__ v, const int64_t* __restrict__ idx, int64_t count,
+                       double2* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = v[idx[i]];
+}
+
+void dist_pack(DistSolver* D, int which, const int64_t* idx, int64_t count, double2* out) {
+    if (count <= 0) return;
+    int64_t len;
+    const double2* v = static_cast<const double2*>(dist_vector(D, which, &len));
+    const int64_t g = (count + 255) / 256;
+    k_pack<<<(unsigned)(g < 4096 ? g : 4096), 256, 0, D->c->stream>>>(v, idx, count, out);
+    ZK_CUDA(cudaGetLastError());
+    D->c->launches++;
+}
+
+void dist_status(DistSolver* D, zk_solve_report* rep, int32_t* done) {
+    SolverState out;
+    cudaStream_t s = D->c->stream;
+    ZK_CUDA(cudaMemcpyAsync(&out, D->P->bufs.st, sizeof(out), cudaMemcpyDeviceToHost, s));
+    ZK_CUDA(cudaStreamSynchronize(s));
+    rep->iterations = out.iterations;
+    rep->converged = out.status == ST_CONVERGED;
+    rep->breakdown = out.status == ST_BREAKDOWN ? out.what : 0;
+    rep->history_len = out.iterations + 1;
+    rep->final_relative_residual = out.last_rel;
+    rep->kernel_launches = 0;
+    *done = out.done ? (out.trivial_zero ? 2 : 1) : 0;
+}
+
+void dist_history(DistSolver* D, double* host, int64_t count) {
+    if (count > D->P->hist_cap) throw ZkError{ZK_ERR_PARAMETER, "history longer than the shard's capacity"};
+    ZK_CUDA(cudaMemcpyAsync(host, D->P->bufs.hist, sizeof(double) * count, cudaMemcpyDeviceToHost, D->c->stream));
+    ZK_CUDA(cudaStreamSynchronize(D->c->stream));
 }
 
 }  // namespace zk

@@ -239,6 +239,29 @@ __device__ __forceinline__ bool warp_finish(const char* plan, const V (&v0)[NACC
     return last != 0;
 }
 
+// Ordered fold of chains continued across calls: lane c (< nchains) adds
+// partials[b*nchains + c] for b < nb to its running total `tot` (first
+// call: first = true starts the chain at partials[c]).  Whole warp.
+__device__ __forceinline__ void warp_fold_cont(const double* partials, int nchains, int64_t nb, double* scratch,
+                                               int chunk, double& tot, bool first) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t c0 = 0; c0 < nb; c0 += chunk) {
+        const int64_t cn = (nb - c0 < chunk) ? nb - c0 : chunk;
+        for (int64_t i = lane; i < cn * nchains; i += 32) scratch[i] = __ldcg(partials + c0 * nchains + i);
+        __syncwarp();
+        if (lane < nchains) {
+            int64_t b = 0;
+            if (first && c0 == 0) {
+                tot = scratch[lane];
+                b = 1;
+            }
+#pragma unroll 16
+            for (; b < cn; ++b) tot = __dadd_rn(tot, scratch[b * nchains + lane]);
+        }
+        __syncwarp();
+    }
+}
+
 // Ordered fold by one warp (vecops.py:159-161): lane c (< nacc*NC) folds the
 // real component chain c; partials are staged through `scratch` (chunk*nacc
 // values).  Result (nacc values) valid in lane 0.

@@ -58,6 +58,7 @@ struct SolverPlan;  // zk_bicgstab.cu
 struct zk_csr {
     zk_context* ctx;
     int64_t n_rows, n_cols, nnz;
+    int64_t nnz_elide;              // nnz numpy's temporary-elision rule sees (the unsharded matrix's)
     int64_t nslices, nblocks;       // 32-row slices, 4096-row blocks
     int64_t sell_elems;             // padded element count
     int32_t wmax;                   // widest slice (entries per row)

@@ -56,7 +56,7 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) 
         const long cap = std::max<long>(10, 180 * 1024 / v.stage_bytes);  // deeper rings measured slower on C4
         v.ns = (int)(ns > std::min<long>(cap, kMaxStages) ? std::min<long>(cap, kMaxStages) : (ns < 1 ? 1 : ns));
         if (env_ns && std::atoi(env_ns) > 0 && std::atoi(env_ns) < v.ns) v.ns = std::atoi(env_ns);
-        v.swap = (A->nnz * 16 >= c->elide_bytes);
+        v.swap = (A->nnz_elide * 16 >= c->elide_bytes);
         v.fma = c->fma != 0;
         v.ns_magic = (uint32_t)((1ull << 32) / (uint64_t)v.ns + 1);
         return v;
@@ -75,7 +75,7 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) 
         if (v.ns >= 20) break;
     }
     if (env_ns && std::atoi(env_ns) > 0 && std::atoi(env_ns) < v.ns) v.ns = std::atoi(env_ns);
-    v.swap = (A->nnz * 16 >= c->elide_bytes);
+    v.swap = (A->nnz_elide * 16 >= c->elide_bytes);
     v.fma = c->fma != 0;
     v.ns_magic = (uint32_t)((1ull << 32) / (uint64_t)v.ns + 1);
     return v;
@@ -180,6 +180,7 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
     A->n_rows = n_rows;
     A->n_cols = n_cols;
     A->nnz = nnz;
+    A->nnz_elide = nnz;
     A->nslices = (n_rows + kSlice - 1) / kSlice;
     A->nblocks = (n_rows + kBlock - 1) / kBlock;
     const int64_t nrp = A->nslices * kSlice;

@@ -574,6 +574,7 @@ struct RedCfg {
     PlanPtrs pc, pr;       // complex / real plans (vecops.py DEFAULT_PLAN, 4096)
     double* partials;      // nblocks x (2 NC + NR) doubles
     unsigned int* counter; // block arrivals (reset by body.finish)
+    int defer;             // row-sharded solve: leave the fold to the cross-rank finish kernel
 };
 
 constexpr int kPlanCache = 2560;  // bytes of shared memory per cached plan (full-block plans: ~2.0 / 1.3 KB)
@@ -808,7 +809,9 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
         }
         last = __shfl_sync(0xffffffffu, last, 0);
         __syncwarp();
-        if (last) {
+        if (last && R.defer) {  // this rank's partials are complete; the ranks fold together
+            if (lane == 0) *R.counter = 0;
+        } else if (last) {
             __threadfence();
             double tot[NP];
             // the stash is free now (every slice of this CTA was reduced): fold scratch
