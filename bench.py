@@ -5,6 +5,9 @@ zSpMV / zdotc GB/s against the HBM roofline.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl zk|reference]
 
 One step = one complete solve (b -> x, tol 1e-8) through the product path.
+With N > 1 (torchrun) the same system is row-sharded over the N GPUs
+(strong scaling, paper_2112_06465_b200/dist.py: halo exchange and block
+partials over NCCL); the result is bit-for-bit the 1-GPU one.
 `value` is timed with CUDA events on the library stream with every input
 resident in HBM; `e2e` repeats the solve through the public Python API with
 the matrix, right-hand side and preconditioner in pinned host memory (the
@@ -60,11 +63,18 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
+        # ZK_BENCH_TRANSPORT=host: ranks share GPU 0 over gloo (exercises the
+        # sharded path on a 1-GPU box; not a performance configuration)
+        self.transport = os.environ.get("ZK_BENCH_TRANSPORT", "nccl")
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            if self.transport == "nccl":
+                torch.cuda.set_device(self.local)
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            else:
+                os.environ["ZK_DEVICE"] = "0"
+                dist.init_process_group("gloo")
             self.dist, self.torch = dist, torch
 
     def barrier(self):
@@ -74,7 +84,8 @@ class Dist:
     def max(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device="cuda")
+        dev = "cuda" if self.transport == "nccl" else "cpu"
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -212,7 +223,7 @@ def run_zk(args, dist: Dist):
     ms_max = dist.max(ms)
     clocks = clk.summary()
     step_ms = ms_max / args.steps
-    value = dist.world * args.steps / (ms_max / 1e3)  # replicas: every rank solves
+    value = args.steps / (ms_max / 1e3)
 
     # ---- e2e: public API, pinned host inputs, fresh upload every step ---------
     pinned = [ia, ja, aa, b, M.data]
@@ -318,7 +329,7 @@ def run_zk(args, dist: Dist):
         "warmup": args.warmup,
         "ms_per_step": round(step_ms, 3),
         "higher_is_better": True,
-        "scaling": "weak" if dist.world > 1 else "strong",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "c128 (f64 re/im pairs)",
         "data": "synthetic: generated 27-point Helmholtz stencil, unit interior source, zero Dirichlet",
@@ -326,11 +337,11 @@ def run_zk(args, dist: Dist):
             "workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8, x0=0",
             "n": n, "nnz": nnz, "iterations": iters, "converged": bool(rep.converged),
             "final_rel": rep.final_relative_residual,
-            "parallelism": f"replicas x{dist.world}" if dist.world > 1 else "1 GPU",
+            "parallelism": "1 GPU",
             "l2": "inputs larger than L2 (4.6 GB matrix, 126 MB L2): no flush",
             "host_setup_s": round(setup_s, 1),
         },
-        "e2e": {"value": round(dist.world / (e2e_step / 1e3), 4), "unit": "solves/s",
+        "e2e": {"value": round(1.0 / (e2e_step / 1e3), 4), "unit": "solves/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": round(e2e_step, 3),
                 "path": "solve_bicgstab(CsrMatrix, ZVector, Preconditioner) from pinned host arrays, x.data read"},
@@ -345,6 +356,104 @@ def run_zk(args, dist: Dist):
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(ia, ja, aa, b, M.data, iters)
+    if dist.rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def run_sharded(args, dist: Dist):
+    """N > 1: the C4 system row-sharded over the N GPUs (strong scaling,
+    paper_2112_06465_b200/dist.py); every rank gets the unsharded bits."""
+    import paper_2112_06465_b200 as Z
+    from paper_2112_06465_b200 import _lib, dist as D
+
+    peak, peak_kind = peaks()
+    t0 = time.time()
+    n, ia, ja, aa, b = build_problem()
+    nnz = int(ia[-1])
+    A = Z.CsrMatrix(n, n, aa, ja, ia, validate=False)
+    M = Z.build_jacobi(A)
+    bounds = D.partition_rows(ia, dist.world)
+    r0, r1 = int(bounds[dist.rank]), int(bounds[dist.rank + 1])
+    lo, hi = int(ia[r0]), int(ia[r1])
+    transport = "nccl" if dist.transport == "nccl" else "host"
+    shard = D.ShardedBiCGStab(bounds, dist.rank, ia[r0:r1 + 1] - lo, ja[lo:hi], aa[lo:hi], nnz, jacobi=True,
+                              max_iterations=MAXIT, transport=transport)
+    b_loc, m_loc = b[r0:r1], M.data[r0:r1]
+    setup_s = time.time() - t0
+    for _ in range(args.warmup):
+        x, rep = shard.solve(b_loc, m_loc, None, TOL, MAXIT)
+    dist.barrier()
+    _lib.synchronize()
+    l0 = Z.launch_count()
+    with Clocks(dist.local) as clk:
+        _lib.event_record(0)
+        for _ in range(args.steps):
+            x, rep = shard.solve(b_loc, m_loc, None, TOL, MAXIT)
+        _lib.event_record(1)
+        ms = _lib.event_elapsed_ms(0, 1)
+    launches = Z.launch_count() - l0
+    _lib.synchronize()
+    dist.barrier()
+    ms_max = dist.max(ms)
+    step_ms = ms_max / args.steps
+    # e2e: the public sharded API from host arrays (partition, shard upload,
+    # halo plan, solve, all-gather of x) every step
+    e2e_ms = []
+    cfg = Z.SolverConfig(tolerance=TOL, max_iterations=MAXIT)
+    for k in range(2):
+        dist.barrier()
+        t1 = time.perf_counter()
+        xe, repe = D.solve_bicgstab_sharded(A, b, M, cfg, transport=transport)
+        e2e_ms.append((time.perf_counter() - t1) * 1e3)
+    e2e_step = dist.max(statistics.median(e2e_ms))
+    assert repe.iterations == rep.iterations
+    # roofline: zSpMV on this rank's shard (own rows, halo columns)
+    xs = Z.ZVector(np.random.default_rng(42).random(shard.n + shard.n_halo) + 0j)
+    Z.spmv(shard.A, xs)
+    _lib.synchronize()
+    _lib.event_record(4)
+    for _ in range(10):
+        Z.spmv(shard.A, xs)
+    _lib.event_record(5)
+    spmv_ms = _lib.event_elapsed_ms(4, 5) / 10
+    snnz = hi - lo
+    sb = 20 * snnz + 4 * (shard.n + 1) + 16 * (shard.n + shard.n_halo) + 16 * shard.n
+    out = {
+        "metric": "bicgstab_solves_per_sec",
+        "value": round(args.steps / (ms_max / 1e3), 4),
+        "unit": "solves/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(step_ms, 3),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "c128 (f64 re/im pairs)",
+        "data": "synthetic: generated 27-point Helmholtz stencil, unit interior source, zero Dirichlet",
+        "config": {
+            "workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8, x0=0",
+            "n": n, "nnz": nnz, "iterations": rep.iterations, "converged": bool(rep.converged),
+            "final_rel": rep.final_relative_residual,
+            "parallelism": f"row-sharded x{dist.world} ({transport}): 4096-aligned nnz-balanced rows, halo "
+                           f"exchange before each SpMV, all-gathered block partials folded in global order",
+            "shard_rows": [int(v) for v in np.diff(bounds)], "halo_rows_rank0": shard.n_halo,
+            "l2": "inputs larger than L2: no flush",
+            "host_setup_s": round(setup_s, 1),
+        },
+        "e2e": {"value": round(1.0 / (e2e_step / 1e3), 4), "unit": "solves/s",
+                "h2d_bytes_per_step": int(20 * nnz + 8 * (n + 1) + 32 * n),
+                "d2h_bytes_per_step": int(16 * n + 8 * (rep.iterations + 1)),
+                "ms_per_step": round(e2e_step, 3),
+                "path": "dist.solve_bicgstab_sharded(CsrMatrix, b, Preconditioner) from host arrays: partition, "
+                        "shard upload, halo plan, solve, all-gather of x"},
+        "roofline": {"bound": "hbm", "kernel": "k_spmv (rank 0 shard)",
+                     "achieved": round(sb / (spmv_ms * 1e-3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(sb / (spmv_ms * 1e-3) / 1e9 / peak, 3), "peak_kind": peak_kind,
+                     "bytes_per_launch": int(sb), "avg_launch_us": round(spmv_ms * 1e3, 1), "traffic": None},
+        "clocks": clk.summary(),
+        "gpu_launches": int(launches),
+    }
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -423,6 +532,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif dist.world > 1:
+            run_sharded(args, dist)
         else:
             run_zk(args, dist)
     finally:
