@@ -66,7 +66,7 @@ class Dist:
         # ZK_BENCH_TRANSPORT=host: ranks share GPU 0 over gloo (exercises the
         # sharded path on a 1-GPU box; not a performance configuration)
         self.transport = os.environ.get("ZK_BENCH_TRANSPORT", "nccl")
-        if self.world > 1:
+        if self.world > 1 or os.environ.get("ZK_BENCH_SHARDED") == "1":  # (1-rank shard: overhead check)
             import torch
             import torch.distributed as dist
             if self.transport == "nccl":
@@ -78,11 +78,11 @@ class Dist:
             self.dist, self.torch = dist, torch
 
     def barrier(self):
-        if self.world > 1:
+        if hasattr(self, "dist"):
             self.dist.barrier()
 
     def max(self, v: float) -> float:
-        if self.world == 1:
+        if not hasattr(self, "dist"):
             return v
         dev = "cuda" if self.transport == "nccl" else "cpu"
         t = self.torch.tensor([v], dtype=self.torch.float64, device=dev)
@@ -90,7 +90,7 @@ class Dist:
         return float(t.item())
 
     def close(self):
-        if self.world > 1:
+        if hasattr(self, "dist"):
             self.dist.destroy_process_group()
 
 
@@ -532,7 +532,7 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, dist)
-        elif dist.world > 1:
+        elif dist.world > 1 or os.environ.get("ZK_BENCH_SHARDED") == "1":
             run_sharded(args, dist)
         else:
             run_zk(args, dist)

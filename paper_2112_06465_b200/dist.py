@@ -278,6 +278,10 @@ class ShardedBiCGStab:
             _lib.check(lib.zk_memcpy_h2d(_lib.context(), ib.ptr, arr.ctypes.data, 8 * len(idx)))
             self._send[q] = (ib, _lib.DeviceBuffer(16 * len(idx)), len(idx))
         self.transport = NcclTransport(group) if transport == "nccl" else HostTransport(group)
+        # NCCL: replay a captured iteration (ZK_DIST_GRAPH=0 issues it op by op)
+        import os
+        self.use_graph = transport == "nccl" and os.environ.get("ZK_DIST_GRAPH", "1") != "0"
+        self._graph = None
 
     def __del__(self):
         try:
@@ -320,6 +324,32 @@ class ShardedBiCGStab:
         _lib.check(_lib.lib().zk_dshard_status(self._h, ctypes.byref(rep), ctypes.byref(done)))
         return rep, done.value
 
+    def _iteration(self) -> None:
+        """One loop iteration (krylov.py:254-294) in the order of the 1-GPU
+        graph; every call is a device-side no-op once the solve stopped."""
+        T = self.transport
+        self._reduce(PH_S_UPDATE)
+        self._phase(PH_X_ALPHA)
+        T.halo(self, DVEC_X)
+        self._reduce(PH_TRUE_RES_S)
+        T.halo(self, DVEC_SHAT)
+        self._reduce(PH_SPMV_T)
+        self._reduce(PH_XR_UPDATE)
+        T.halo(self, DVEC_X)
+        self._reduce(PH_TRUE_RES)
+        self._phase(PH_P_NEXT)
+        T.halo(self, DVEC_PHAT)
+        self._reduce(PH_PIVOT)
+
+    def _capture(self):
+        """CUDA graph of one iteration -- kernels and NCCL ops on libzk's
+        stream -- so the host issues one launch per iteration."""
+        import torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.transport.stream):
+            self._iteration()
+        return g
+
     # -- the loop -----------------------------------------------------------------
     def solve(self, b_local, minv_local=None, x0_local=None, tolerance: float = 1e-9,
               max_iterations: int = 1000, check_every: int = 8):
@@ -341,21 +371,14 @@ class ShardedBiCGStab:
             self._phase(PH_P_FIRST)
             T.halo(self, DVEC_PHAT)
             self._reduce(PH_PIVOT)
+            step = self._iteration
+            if self.use_graph:
+                if self._graph is None:
+                    self._graph = self._capture()  # captured, not executed
+                step = self._graph.replay
             it = 0
             while True:
-                # one iteration (krylov.py:254-294); device-side no-ops once stopped
-                self._reduce(PH_S_UPDATE)
-                self._phase(PH_X_ALPHA)
-                T.halo(self, DVEC_X)
-                self._reduce(PH_TRUE_RES_S)
-                T.halo(self, DVEC_SHAT)
-                self._reduce(PH_SPMV_T)
-                self._reduce(PH_XR_UPDATE)
-                T.halo(self, DVEC_X)
-                self._reduce(PH_TRUE_RES)
-                self._phase(PH_P_NEXT)
-                T.halo(self, DVEC_PHAT)
-                self._reduce(PH_PIVOT)
+                step()
                 it += 1
                 if it % check_every == 0 or it >= max_iterations:
                     rep, done = self._status()
