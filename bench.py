@@ -38,9 +38,23 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG = "C4"
+CONFIG = "C4"  # the headline; --config C1|C3|C5 runs the other BASELINE systems
+WORKLOADS = {
+    "C1": "C1: 7-point Helmholtz FD 32^3 (cells=33, frequency 1.5), Jacobi BiCGStab tol 1e-8, x0=0 "
+          "(the reference's CPU path)",
+    "C3": "C3: cylinder P1-FE Helmholtz (996,369 rows, 14.7M nnz; k=4pi, eps=0.1, point source), "
+          "Jacobi BiCGStab tol 1e-8, x0=0",
+    "C4": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8, x0=0",
+    "C5": "C5: 7-point Helmholtz FD 256^3, 12 points per wavelength, eps=0.3, Jacobi BiCGStab tol 1e-8, x0=0",
+}
+DATA = {
+    "C1": "synthetic: reference 7-point FD assembly (bitwise helmholtz.assemble), unit interior source",
+    "C3": "synthetic: generated P1 tetrahedral FE cylinder (Kuhn split), unit point source",
+    "C4": "synthetic: generated 27-point Helmholtz stencil, unit interior source, zero Dirichlet",
+    "C5": "synthetic: generated 7-point FD stencil, complex damping, unit interior source",
+}
 TOL = 1e-8
-MAXIT = 5000
+MAXIT = 20000
 # Iterations of the C4 solve (bitwise identical between this GPU path and the
 # reference algorithm; the GPU arm re-measures it every run and reports both).
 C4_ITERATIONS_KNOWN = 215  # measured on B200 (bench r01), bitwise the reference algorithm
@@ -193,7 +207,7 @@ def run_zk(args, dist: Dist):
 
     peak, peak_kind = peaks()
     t0 = time.time()
-    n, ia, ja, aa, b = build_problem()
+    n, ia, ja, aa, b = build_problem(args.config)
     nnz = int(ia[-1])
     A = Z.CsrMatrix(n, n, aa, ja, ia)
     M = Z.build_jacobi(A)
@@ -332,9 +346,9 @@ def run_zk(args, dist: Dist):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "c128 (f64 re/im pairs)",
-        "data": "synthetic: generated 27-point Helmholtz stencil, unit interior source, zero Dirichlet",
+        "data": DATA[args.config],
         "config": {
-            "workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8, x0=0",
+            "workload": WORKLOADS[args.config],
             "n": n, "nnz": nnz, "iterations": iters, "converged": bool(rep.converged),
             "final_rel": rep.final_relative_residual,
             "parallelism": "1 GPU",
@@ -355,7 +369,7 @@ def run_zk(args, dist: Dist):
         "sub_metrics": sub,
     }
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(ia, ja, aa, b, M.data, iters)
+        out["cpu_baseline"] = cpu_baseline(ia, ja, aa, b, M.data, iters, args.config)
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -368,7 +382,7 @@ def run_sharded(args, dist: Dist):
 
     peak, peak_kind = peaks()
     t0 = time.time()
-    n, ia, ja, aa, b = build_problem()
+    n, ia, ja, aa, b = build_problem(args.config)
     nnz = int(ia[-1])
     A = Z.CsrMatrix(n, n, aa, ja, ia, validate=False)
     M = Z.build_jacobi(A)
@@ -430,9 +444,9 @@ def run_sharded(args, dist: Dist):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "c128 (f64 re/im pairs)",
-        "data": "synthetic: generated 27-point Helmholtz stencil, unit interior source, zero Dirichlet",
+        "data": DATA[args.config],
         "config": {
-            "workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8, x0=0",
+            "workload": WORKLOADS[args.config],
             "n": n, "nnz": nnz, "iterations": rep.iterations, "converged": bool(rep.converged),
             "final_rel": rep.final_relative_residual,
             "parallelism": f"row-sharded x{dist.world} ({transport}): 4096-aligned nnz-balanced rows, halo "
@@ -470,12 +484,12 @@ def cpu_sample(ia, ja, aa, b, minv, iters):
     return 1.0 / per_solve, {"setup_s": t_setup, "iteration_s": t_iter, "wall_s": wall, "hist1": hist[-1]}
 
 
-def cpu_baseline(ia, ja, aa, b, minv, iters):
+def cpu_baseline(ia, ja, aa, b, minv, iters, config=CONFIG):
     from oracle import fingerprint
     v, d = cpu_sample(ia, ja, aa, b, minv, iters)
     facts = fingerprint.host_facts()
     return {"value": v, "unit": "solves/s", "cores": 1, "kind": "port",
-            "sample": (f"reference BiCGStab algorithm (oracle/port.py, numpy, single-threaded like zlinalg) on C4: "
+            "sample": (f"reference BiCGStab algorithm (oracle/port.py, numpy, single-threaded like zlinalg) on {config}: "
                        f"setup {d['setup_s']:.2f}s + 1 iteration {d['iteration_s']:.2f}s, extrapolated to "
                        f"{iters} iterations"),
             "host": facts}
@@ -527,6 +541,7 @@ def main():
     ap.add_argument("--impl", choices=["zk", "reference"], default="zk")
     ap.add_argument("--iterations", type=int, default=None, help="reference arm: C4 iteration count")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default=CONFIG, help="BASELINE system (default C4)")
     args = ap.parse_args()
     dist = Dist() if args.impl == "zk" else _NoDist()
     try:

@@ -15,6 +15,8 @@ replacements for the reference's per-row Python loop
   damping ``k^2 (1 + i eps)``; BASELINE configs C1/C5).
 * :func:`helmholtz_27pt` -- 27-point stencil, diagonal ``26/(3h^2) - k^2(1+i eps)``,
   off-diagonals ``-1/(3h^2)`` (BASELINE config C4).
+* :func:`cylinder_p1fe` -- P1 tetrahedral FE Helmholtz on a cylinder (BASELINE
+  config C3; irregular FE rows, up to 15 nonzeros).
 * :func:`config_problem` -- the named BASELINE configurations.
 """
 from __future__ import annotations
@@ -23,7 +25,7 @@ import math
 
 import numpy as np
 
-__all__ = ["helmholtz_fd", "helmholtz_27pt", "config_problem", "CONFIGS"]
+__all__ = ["helmholtz_fd", "helmholtz_27pt", "cylinder_p1fe", "config_problem", "CONFIGS"]
 
 
 def _csr_from_mask(mask: np.ndarray, cols: np.ndarray, vals: np.ndarray):
@@ -110,10 +112,91 @@ def helmholtz_27pt(m: int, k2: float = 100.0, damping: float = 0.05, length: flo
     return n, ia, ja, aa, b
 
 
+def cylinder_p1fe(m: int, length: float = 2.0, wavelengths: float = 2.0, damping: float = 0.1,
+                  source: complex = 1 + 0j):
+    """P1 finite-element Helmholtz system on a cylinder (BASELINE config C3,
+    "cylinder-like synthetic P1-FE"; the paper's Cylinder3D matrices are not
+    available).  Grid spacing h = 2/m over [-1, 1]^2 x [0, length], Kuhn
+    split of every cube into 6 congruent tetrahedra, tetrahedra kept when all
+    four vertices lie in the unit-radius cylinder; ``A = K - k^2 (1 + i eps) M``
+    with P1 stiffness K and consistent mass M, natural (Neumann) boundary, and
+    ``k = 2*pi*wavelengths``; unit point source at the node nearest the axis
+    midpoint.  Interior rows have 15 nonzeros (the Kuhn 15-point stencil),
+    boundary rows fewer -- the irregular row lengths of an FE matrix.
+    Returns ``(n, ia, ja, aa, b)``; columns ascend in each row.
+    """
+    import scipy.sparse as sp
+    h = 2.0 / m
+    mz = int(round(length / h))
+    nx, ny, nz = m + 1, m + 1, mz + 1
+    gx = -1.0 + h * np.arange(nx)
+    inside2d = (gx[:, None] ** 2 + gx[None, :] ** 2) <= 1.0 + 1e-12  # [ix, iy]
+    # Kuhn tetrahedra of the unit cube: vertex sequences 0 -> e_a -> e_a+e_b -> (1,1,1)
+    import itertools
+    cube = {}
+    tets = []
+    for perm in itertools.permutations(range(3)):
+        v = [np.zeros(3, dtype=np.int64)]
+        for a in perm:
+            w = v[-1].copy()
+            w[a] = 1
+            v.append(w)
+        tets.append(np.stack(v))
+    # element matrices (all six tetrahedra are congruent up to reflection)
+    ke, me = [], []
+    for tv in tets:
+        X = tv.astype(np.float64) * h
+        T = np.vstack([np.ones(4), X.T])  # 4x4
+        Ginv = np.linalg.inv(T)          # rows: barycentric coefficient vectors
+        grads = Ginv[:, 1:]              # (4, 3)
+        vol = abs(np.linalg.det(T)) / 6.0
+        ke.append(vol * grads @ grads.T)
+        me.append(vol / 20.0 * (np.ones((4, 4)) + np.eye(4)))
+    k2 = (2.0 * math.pi * wavelengths) ** 2
+    shift = complex(k2, k2 * damping)
+    # cube origins (ix, iy, iz) with all corners inside the cylinder
+    cx, cy = np.nonzero(inside2d[:-1, :-1] & inside2d[1:, :-1] & inside2d[:-1, 1:] & inside2d[1:, 1:])
+    if cx.size == 0:
+        raise ValueError("grid too coarse for the cylinder")
+    cz = np.arange(nz - 1, dtype=np.int64)
+    ox = np.repeat(cx, cz.size)
+    oy = np.repeat(cy, cz.size)
+    oz = np.tile(cz, cx.size)
+    gid = lambda x, y, z: (z * ny + y) * nx + x  # noqa: E731  (lexicographic grid id, x fastest)
+    rows, cols, vals = [], [], []
+    for t, tv in enumerate(tets):
+        nodes = [gid(ox + tv[a, 0], oy + tv[a, 1], oz + tv[a, 2]) for a in range(4)]
+        loc = ke[t] - shift * me[t]
+        for a in range(4):
+            for c in range(4):
+                rows.append(nodes[a])
+                cols.append(nodes[c])
+                vals.append(np.full(ox.size, loc[a, c], dtype=np.complex128))
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    vals = np.concatenate(vals)
+    used = np.unique(rows)
+    remap = np.full(nx * ny * nz, -1, dtype=np.int64)
+    remap[used] = np.arange(used.size, dtype=np.int64)
+    n = int(used.size)
+    A = sp.coo_matrix((vals, (remap[rows], remap[cols])), shape=(n, n)).tocsr()
+    A.sum_duplicates()
+    A.sort_indices()
+    ia = A.indptr.astype(np.int64)
+    ja = A.indices.astype(np.int64)
+    aa = np.ascontiguousarray(A.data, dtype=np.complex128)
+    # point source nearest the axis midpoint
+    mid = gid(int(np.argmin(np.abs(gx))), int(np.argmin(np.abs(gx))), nz // 2)
+    b = np.zeros(n, dtype=np.complex128)
+    b[remap[mid] if remap[mid] >= 0 else n // 2] = complex(source)
+    return n, ia, ja, aa, b
+
+
 # Named BASELINE.json configurations (SURVEY 8d).  C1 is exactly the reference
 # CPU path: load_problem_config-style dim=3, cells=33, frequency=1.5 (k = 3*pi).
 CONFIGS = {
     "C1": dict(kind="fd", dim=3, cells=33, frequency=1.5, damping=0.0, tol=1e-8),
+    "C3": dict(kind="p1fe", m=108, length=2.0, wavelengths=2.0, damping=0.1, tol=1e-8),
     "C4": dict(kind="27pt", m=200, k2=100.0, damping=0.05, tol=1e-8),
     "C5": dict(kind="fd", dim=3, cells=257, frequency=257 / 12.0, damping=0.3, tol=1e-8),
 }
@@ -127,4 +210,6 @@ def config_problem(name: str, scale: int | None = None):
         freq = c["frequency"] if not scale or name != "C5" else cells / 12.0
         return helmholtz_fd(c["dim"], cells, frequency=freq, damping=c["damping"])
     m = scale or c["m"]
+    if c["kind"] == "p1fe":
+        return cylinder_p1fe(m, c["length"], c["wavelengths"], c["damping"])
     return helmholtz_27pt(m, k2=c["k2"], damping=c["damping"])

@@ -121,12 +121,15 @@ def test_bicgstab_golden(bicgstab_golden):
         assert bits(x.data) == bits(g["x"]), case
 
 
-@pytest.mark.parametrize("shape", [("fd", 49, 49 / 12.0, 0.3), ("s27", 30, 0, 0), ("fd", 65, 3.0, 0.0)])
+@pytest.mark.parametrize("shape", [("fd", 49, 49 / 12.0, 0.3), ("s27", 30, 0, 0), ("fd", 65, 3.0, 0.0),
+                                   ("fe", 24, 0, 0)])
 def test_bicgstab_vs_oracle_multiblock(shape):
     """Larger systems (many 4096-row blocks, partial tail block) vs the C oracle."""
     kind, m, freq, eps = shape
     if kind == "fd":
         n, ia, ja, aa, b = problems.helmholtz_fd(3, m, frequency=freq, damping=eps)
+    elif kind == "fe":  # BASELINE C3 shape (P1-FE cylinder), irregular rows
+        n, ia, ja, aa, b = problems.cylinder_p1fe(m)
     else:
         n, ia, ja, aa, b = problems.helmholtz_27pt(m, k2=100.0, damping=0.05)
     A = Z.CsrMatrix(n, n, aa, ja, ia)
@@ -134,6 +137,21 @@ def test_bicgstab_vs_oracle_multiblock(shape):
     x, rep = Z.solve_bicgstab(A, Z.ZVector(b), M, Z.SolverConfig(tolerance=1e-8, max_iterations=3000))
     xo, hist, it, st, _ = O.bicgstab(n, ia, ja, aa, b, M.data, None, 1e-8, 3000)
     assert rep.iterations == it
+    assert np.array(rep.residual_history).tobytes() == np.array(hist).tobytes()
+    assert bits(x.data) == bits(xo)
+
+
+def test_c3_spmv_and_capped_solve_vs_oracle():
+    """BASELINE C3 itself (996k rows, 14.7M nnz): SpMV and a capped solve, bitwise."""
+    n, ia, ja, aa, b = problems.config_problem("C3")
+    A = Z.CsrMatrix(n, n, aa, ja, ia, validate=False)
+    rng = np.random.default_rng(5)
+    xv = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    assert bits(Z.spmv(A, Z.ZVector(xv)).data) == bits(O.spmv(n, n, ia, ja, aa, xv))
+    M = Z.build_jacobi(A)
+    x, rep = Z.solve_bicgstab(A, Z.ZVector(b), M, Z.SolverConfig(tolerance=1e-8, max_iterations=20))
+    xo, hist, it, st, _ = O.bicgstab(n, ia, ja, aa, b, M.data, None, 1e-8, 20)
+    assert rep.iterations == it == 20
     assert np.array(rep.residual_history).tobytes() == np.array(hist).tobytes()
     assert bits(x.data) == bits(xo)
 
