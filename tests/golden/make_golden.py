@@ -2,7 +2,7 @@
 
 Run in the dev container (where /root/reference exists):
 
-    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py [krylov_ext]
 
 It imports ``zlinalg`` from ``/root/reference/pkg/src`` read-only, feeds it
 seeded inputs, and writes compressed ``.npz`` fixtures next to this script.
@@ -206,6 +206,43 @@ def solver_goldens():
     return out
 
 
+def krylov_ext_goldens():
+    """BiCGSTAB(l) (l = 2, 8) and TFQMR (krylov.py:298-489) on a subset of the
+    BiCGStab cases, for tests/test_krylov_ext_gpu.py."""
+    keep = {"fd9", "fd13", "damped21", "s27_14", "dom50_310", "dom200_320", "dom40_identity", "dom80_maxit3",
+            "dom30_guess", "ident5", "zero_rhs", "rotation"}
+    out = {}
+    for name, A, b, prec, tol, maxit, guess in solver_cases():
+        if name not in keep:
+            continue
+        M = Z.build_jacobi(A) if prec == "jacobi" else Z.Preconditioner.identity()
+        for solver, ell in (("bicgstabl", 2), ("bicgstabl", 8), ("tfqmr", 8)):
+            tag = f"{name}_{solver}{ell if solver == 'bicgstabl' else ''}"
+            cfg = Z.SolverConfig(tolerance=tol, max_iterations=maxit, l=ell,
+                                 initial_guess=Z.ZVector(guess.copy()) if guess is not None else None)
+            fn = Z.solve_bicgstab_l if solver == "bicgstabl" else Z.solve_tfqmr
+            status, what = "converged", ""
+            try:
+                x, rep = fn(A, Z.ZVector(np.asarray(b, dtype=np.complex128).copy()), M, cfg)
+                if not rep.converged:
+                    status = "not_converged"
+                xd = x.data
+            except Z.BreakdownError as e:
+                rep, status, what, xd = e.report, "breakdown", str(e), np.zeros(0, dtype=np.complex128)
+            out[f"{tag}__ia"], out[f"{tag}__ja"], out[f"{tag}__aa"] = A.ia, A.ja, A.aa
+            out[f"{tag}__b"] = np.asarray(b, dtype=np.complex128)
+            out[f"{tag}__minv"] = M.data if prec == "jacobi" else np.zeros(0, dtype=np.complex128)
+            out[f"{tag}__guess"] = guess if guess is not None else np.zeros(0, dtype=np.complex128)
+            out[f"{tag}__params"] = np.array([tol, maxit, ell])
+            out[f"{tag}__solver"] = np.array([solver])
+            out[f"{tag}__x"] = xd
+            out[f"{tag}__hist"] = np.array(rep.residual_history)
+            out[f"{tag}__status"] = np.array([status])
+            out[f"{tag}__what"] = np.array([what])
+            print(f"  {tag}: n={A.n_rows} {status} it={rep.iterations} rel={rep.final_relative_residual:.3e}")
+    return out
+
+
 def problem_goldens():
     out = {}
     for dim, cells, freq in ((1, 12, 0.7), (2, 11, 1.1), (3, 9, 1.0), (3, 13, 1.5)):
@@ -218,6 +255,9 @@ def problem_goldens():
 
 
 def main():
+    if sys.argv[1:] == ["krylov_ext"]:  # add the BiCGSTAB(l)/TFQMR fixtures only
+        np.savez_compressed(os.path.join(HERE, "krylov_ext.npz"), **krylov_ext_goldens())
+        return
     from numpy._core._multiarray_umath import __cpu_dispatch__, __cpu_baseline__
     meta = dict(numpy=np.__version__, python=sys.version.split()[0], cpu_baseline=list(__cpu_baseline__),
                 cpu_dispatch=list(__cpu_dispatch__), reference=REF, generator=os.path.basename(__file__))
@@ -229,6 +269,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "problems.npz"), **problem_goldens())
     print("solvers ...")
     np.savez_compressed(os.path.join(HERE, "bicgstab.npz"), **solver_goldens())
+    np.savez_compressed(os.path.join(HERE, "krylov_ext.npz"), **krylov_ext_goldens())
     with open(os.path.join(HERE, "meta.json"), "w") as fh:
         json.dump(meta, fh, indent=1)
 
