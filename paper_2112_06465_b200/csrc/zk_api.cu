@@ -6,12 +6,6 @@
 #include <vector>
 
 #include "zk_internal.h"
-#if defined(ZK_EXP) && ZK_EXP >= 10
-namespace zk {
-void debug_read_spmv(unsigned long long* out, bool reset);
-void debug_read_solver(unsigned long long* out, bool reset);
-}  // namespace zk
-#endif
 
 namespace zk {
 
@@ -303,14 +297,6 @@ zk_status zk_memset(zk_context* c, void* dst, int value, size_t bytes) {
     });
 }
 
-#if defined(ZK_EXP) && ZK_EXP >= 10
-extern "C" zk_status zk_debug_read(unsigned long long* out, int reset, int solver) {
-    return guarded([&] {
-        if (solver) zk::debug_read_solver(out, reset != 0);
-        else zk::debug_read_spmv(out, reset != 0);
-    });
-}
-#endif
 
 zk_status zk_synchronize(zk_context* c) {
     return guarded([&] {

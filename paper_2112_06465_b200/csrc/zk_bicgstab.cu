@@ -615,16 +615,6 @@ void build_graph(const Launch& L) {
 
 }  // namespace
 
-#if defined(ZK_EXP) && ZK_EXP >= 10
-void debug_read_solver(unsigned long long* out, bool reset) {
-    ZK_CUDA(cudaDeviceSynchronize());
-    ZK_CUDA(cudaMemcpyFromSymbol(out, zk_dbg, sizeof(unsigned long long) * 16));
-    if (reset) {
-        unsigned long long z[16] = {};
-        ZK_CUDA(cudaMemcpyToSymbol(zk_dbg, z, sizeof(z)));
-    }
-}
-#endif
 
 void destroy_solver_plan(zk_context* c, SolverPlan* P) {
     if (!P) return;

@@ -260,16 +260,6 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
     return A;
 }
 
-#if defined(ZK_EXP) && ZK_EXP >= 10
-void debug_read_spmv(unsigned long long* out, bool reset) {
-    ZK_CUDA(cudaDeviceSynchronize());
-    ZK_CUDA(cudaMemcpyFromSymbol(out, zk_dbg, sizeof(unsigned long long) * 16));
-    if (reset) {
-        unsigned long long z[16] = {};
-        ZK_CUDA(cudaMemcpyToSymbol(zk_dbg, z, sizeof(z)));
-    }
-}
-#endif
 
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
     if (A->n_rows == 0) return;
@@ -277,10 +267,7 @@ void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
         ZK_CUDA(cudaMemsetAsync(y, 0, sizeof(double2) * A->n_rows, c->stream));
         return;
     }
-    const char* e_nsv = std::getenv("ZK_EXP_NSV");  // experiment: stage x rows with every slice
-    const int nsv = e_nsv ? std::atoi(e_nsv) : 0;
-    SellView v = sell_view(A, c, 0, nsv);
-    v.sv[0] = v.sv[1] = x;
+    const SellView v = sell_view(A, c, 0, 0);
     const size_t smem = pipe_smem_bytes(v, 0);
     ZK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_spmv<<<pipe_grid(A), kPipeThreads, smem, c->stream>>>(v, x, y);

@@ -64,12 +64,6 @@ constexpr int kStashSlices = 32;
 constexpr int kStashMask = kStashSlices * kSlice - 1;
 constexpr int kNodeSlots = 136;  // >= plan nodes (<= 129) per accumulator
 
-#if defined(ZK_EXP) && ZK_EXP >= 10
-static __device__ unsigned long long zk_dbg[16];  // per translation unit
-#if ZK_EXP >= 11
-__shared__ long long zk_dbg_sh[32];
-#endif
-#endif
 
 struct SellView {
     int64_t n_rows, n_cols, nslices, nblocks;
@@ -371,19 +365,9 @@ __device__ __forceinline__ void uni_seg(const double2* __restrict__ x, const dou
     double2 xs[K1 - K0];
 #pragma unroll
     for (int k = K0; k < K1; ++k) xs[k - K0] = __ldg(x + sja[32 * k + lane]);
-#if defined(ZK_EXP) && ZK_EXP >= 11
-    if (K0 == 0 && lane == 0) zk_dbg_sh[(threadIdx.x >> 5) * 2] = clock64();
-#endif
 #pragma unroll
     for (int k = K0; k < K1; ++k) {
         const double2 p = prod_fma<SWAP>(saa[32 * k + lane], xs[k - K0]);
-#if defined(ZK_EXP) && ZK_EXP >= 11
-        if (k == 0) {
-            double px = p.x;
-            asm volatile("" : "+d"(px));
-            if (lane == 0 && px != 12345.678) zk_dbg_sh[(threadIdx.x >> 5) * 2 + 1] = clock64();
-        }
-#endif
         if (k == 0) {
             v0 = p;
         } else {
@@ -757,11 +741,6 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
             }
             int need = (int)nrows;  // first block row a pending leaf still reads
             bool worked = false;
-#if defined(ZK_EXP) && ZK_EXP >= 1 && ZK_EXP < 10  // timing experiment: no leaf work (wrong results)
-            if (lane == 0) mbar_arrive(&sm.sfree()[sq % kStashSlices]);
-            rel = j + 1;
-            continue;
-#endif
             if constexpr (NC > 0) {
                 const int hi = lastj ? nlc : min((int)hc->leaf_upto[j + 1], nlc);
                 if (hi - lc >= kBatchC || (lastj && hi > lc)) {
@@ -914,19 +893,12 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
                     const uint32_t cnt = (uint32_t)w * kSlice;
                     const int64_t r0 = s * kSlice;
                     const uint32_t vrows = (uint32_t)min((int64_t)kSlice, A.n_rows - r0);
-#if defined(ZK_EXP) && ZK_EXP >= 2 && ZK_EXP < 10
-                    mbar_arrive_expect_tx(&full[lane], cnt * 20u + kSlice);
-#else
                     mbar_arrive_expect_tx(&full[lane], cnt * 20u + kSlice + (uint32_t)A.nsv * vrows * 16u);
-#endif
                     if (cnt) {
                         bulk_g2s(stage, A.aa + off0, cnt * 16u, &full[lane], pol);
                         bulk_g2s(stage + A.ja_off, A.ja + off0, cnt * 4u, &full[lane], pol);
                     }
                     bulk_g2s(stage + A.rl_off, A.rowlen + r0, kSlice, &full[lane], pol);
-#if defined(ZK_EXP) && ZK_EXP >= 2 && ZK_EXP < 10
-                    if (0)
-#endif
                     for (int v = 0; v < A.nsv; ++v)
                         bulk_g2s(stage + A.sv_off + v * kSlice * 16, A.sv[v] + r0, vrows * 16u, &full[lane], pol);
                 } else {
@@ -954,9 +926,6 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
     }
     // ---- consumer warps: warp w takes slices w, w+kCW, ... of each block ----
     const bool fast = A.cm == 0 && A.fma;
-#if defined(ZK_EXP) && ZK_EXP >= 10
-    unsigned long long dbg_wait = 0, dbg_comp = 0, dbg_n = 0, dbg_uni = 0, dbg_iss = 0, dbg_lat = 0, dbg_rest = 0;
-#endif
     uint32_t sbase = 0;  // CTA-local index of the block's first slice
     for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
         const int64_t s_lo = blk * kSlicesPerBlock;
@@ -971,48 +940,22 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             RowVals<NX> val;
             int len;
             if (fast) {
-#if defined(ZK_EXP) && ZK_EXP >= 10
-                const long long t0 = clock64();
-#endif
                 const uint32_t q = __umulhi(sq, A.ns_magic);
                 const int st = (int)(sq - q * (uint32_t)ns);
                 while (tag[st] != sq) {
                 }
                 mbar_wait(&full[st], q & 1);
-#if defined(ZK_EXP) && ZK_EXP >= 10
-                const long long t1 = clock64();
-#endif
                 const unsigned char* stage = ring + (size_t)st * A.stage_bytes;
                 const int W = (int)wid[st];
                 len = stage[A.rl_off + lane];
                 val = row_fast_dispatch<SWAP, NX>(W, x0, x1, reinterpret_cast<const double2*>(stage),
                                                   reinterpret_cast<const int32_t*>(stage + A.ja_off), lane,
                                                   (mine && len != 255) ? len : 0, !mine);
-#if defined(ZK_EXP) && ZK_EXP >= 2 && ZK_EXP < 10
-#pragma unroll
-                for (int v = 0; v < SV; ++v) svals[v] = A.sv[v][mine ? row : 0];
-#else
 #pragma unroll
                 for (int v = 0; v < SV; ++v)
                     svals[v] = reinterpret_cast<const double2*>(stage + A.sv_off)[v * kSlice + lane];
-#endif
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
-#if defined(ZK_EXP) && ZK_EXP >= 10
-                const long long t2 = clock64();
-                const bool uni = __all_sync(0xffffffffu, !mine || len == W);
-                dbg_wait += t1 - t0;
-                dbg_comp += t2 - t1;
-#if ZK_EXP >= 11
-                if (uni) {
-                    dbg_iss += zk_dbg_sh[warp * 2] - t1;
-                    dbg_lat += zk_dbg_sh[warp * 2 + 1] - zk_dbg_sh[warp * 2];
-                    dbg_rest += t2 - zk_dbg_sh[warp * 2 + 1];
-                }
-#endif
-                dbg_n += 1;
-                dbg_uni += uni ? 1 : 0;
-#endif
             } else {
                 len = A.rowlen[row];
                 val = generic_slice<NX>(A, x0, x1, full, empty, tag, ring, sq, lane, (mine && len != 255) ? len : 0);
@@ -1042,18 +985,6 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
         }
         sbase += (uint32_t)nsl;
     }
-#if defined(ZK_EXP) && ZK_EXP >= 10
-    if (lane == 0) {
-        atomicAdd(&zk_dbg[0], dbg_wait);
-        atomicAdd(&zk_dbg[1], dbg_comp);
-        atomicAdd(&zk_dbg[2], dbg_n);
-        atomicAdd(&zk_dbg[6], dbg_uni);
-        atomicAdd(&zk_dbg[5], dbg_n - dbg_uni);
-        atomicAdd(&zk_dbg[7], dbg_iss);
-        atomicAdd(&zk_dbg[8], dbg_lat);
-        atomicAdd(&zk_dbg[9], dbg_rest);
-    }
-#endif
 }
 
 // Kernel-side dispatch on numpy's elision swap (a launch-uniform flag).

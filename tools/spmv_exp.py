@@ -1,5 +1,5 @@
-"""SpMV bottleneck experiments on C4 (env ZK_SPMV_EXP: 0 normal, 1 L1-resident
-gathers, 2 no consumer work = pure TMA stream; ZK_NS ring depth)."""
+"""Standalone zSpMV on C4 across ring depths (env ZK_NS caps the stage count;
+NSS lists the depths to time)."""
 import json
 import os
 import sys
@@ -16,9 +16,9 @@ A = Z.CsrMatrix(n, n, aa, ja, ia)
 x = Z.ZVector(np.random.default_rng(0).random(n) + 0j)
 bytes_ = 20 * ia[-1] + 4 * (n + 1) + 32 * n
 res = {}
-for exp in os.environ.get("EXPS", "0").split(","):
+for exp in ("0",):
     for ns in os.environ.get("NSS", "4,6,8,10,12").split(","):
-        os.environ["ZK_SPMV_EXP"], os.environ["ZK_NS"] = exp, ns
+        os.environ["ZK_NS"] = ns
         Z.spmv(A, x)
         _lib.synchronize()
         _lib.event_record(0)
