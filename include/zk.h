@@ -134,6 +134,12 @@ zk_status zk_csr_destroy(zk_csr* A);
 zk_status zk_csr_bytes(const zk_csr* A, int64_t* bytes, int64_t* padded_elems);
 /* y <- A x (x: n_cols, y: n_rows)               replaces sparse.spmv (sparse.py:217-232) */
 zk_status zk_spmv(zk_context* ctx, const zk_csr* A, const double* x, double* y);
+/* y <- A x and result = sum cbar(w)*y in ONE pass over A (the SpMV's rows feed
+ * the DEFAULT_PLAN block reduction as they are produced): bitwise
+ * sparse.spmv(A, x) followed by vecops.zdot(w, y, conjugate) (vecops.py:165-186),
+ * the fusion the BiCGStab loop uses for its shadow pivot (krylov.py:267-268). */
+zk_status zk_spmv_dotc(zk_context* ctx, const zk_csr* A, const double* x, double* y, const double* w,
+                       int conjugate, double* result_host);
 
 /* ---- BiCGStab (krylov.py) ----------------------------------------------- */
 typedef struct {

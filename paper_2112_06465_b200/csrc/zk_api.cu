@@ -107,6 +107,8 @@ void dist_finish(DistSolver* D, int phase, const int64_t* rank_blocks);
 void dist_pack(DistSolver* D, int which, const int64_t* idx, int64_t count, double2* out);
 void dist_status(DistSolver* D, zk_solve_report* rep, int32_t* done);
 void dist_history(DistSolver* D, double* host, int64_t count);
+void spmv_dot_device(zk_context* c, const zk_csr* A, const double2* x, double2* y, const double2* w, bool conj,
+                     double2* result);
 int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
                     int64_t maxit, double2* x_out, double* history_host, zk_solve_report* rep);
 void destroy_solver_plan(zk_context* c, SolverPlan* P);
@@ -537,6 +539,27 @@ zk_status zk_csr_bytes(const zk_csr* A, int64_t* bytes, int64_t* padded) {
         if (A->n_long) b += A->n_long * 4 + (A->nblocks + 1) * 4 + (A->n_long + 1) * 8;
         *bytes = b;
         *padded = A->sell_elems;
+    });
+}
+
+zk_status zk_spmv_dotc(zk_context* c, const zk_csr* A, const double* x, double* y, const double* w, int conjugate,
+                       double* result_host) {
+    return guarded([&] {
+        need_ctx(c);
+        need(A != nullptr, ZK_ERR_PARAMETER, "null matrix");
+        need(result_host != nullptr, ZK_ERR_PARAMETER, "null result");
+        if (A->n_rows == 0) {  // empty y: zdot of empty vectors is (0, 0) (vecops.py:173-174)
+            result_host[0] = result_host[1] = 0.0;
+            return;
+        }
+        need_ptr(x, A->n_cols, "x");
+        need_ptr(y, A->n_rows, "y");
+        need_ptr(w, A->n_rows, "w");
+        spmv_dot_device(c, A, D2(x), D2(y), D2(w), conjugate != 0, reinterpret_cast<double2*>(c->d_result));
+        ZK_CUDA(cudaMemcpyAsync(c->h_result, c->d_result, sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+        ZK_CUDA(cudaStreamSynchronize(c->stream));
+        result_host[0] = c->h_result[0];
+        result_host[1] = c->h_result[1];
     });
 }
 

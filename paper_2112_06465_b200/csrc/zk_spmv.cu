@@ -155,6 +155,31 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv(SellView A, const doub
     sell_run<1>(A, x, nullptr, body, R, smem);
 }
 
+// y = A x fused with <w, y> (DEFAULT_PLAN blocks over y): sparse.spmv then
+// vecops.zdot(w, y), bit for bit, in one pass over the matrix.
+struct SpmvDotBody {
+    static constexpr int kNC = 1, kNR = 0, kSV = 1;  // staged: w
+    double2* __restrict__ y;
+    double2* result;
+    unsigned int* counter;
+    bool conj, fma;
+    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[1], const double2 (&w)[1], double2 (&tc)[1],
+                                        double (&)[1]) {
+        y[r] = v[0];
+        tc[0] = f1(conj ? conjz(w[0]) : w[0], v[0], fma);
+    }
+    __device__ void finish(const double* t) {
+        *result = make_double2(t[0], t[1]);
+        *counter = 0;
+    }
+};
+
+__global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_dot(SellView A, const double2* __restrict__ x,
+                                                                 SpmvDotBody body, RedCfg R) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    sell_run<1>(A, x, nullptr, body, R, smem);
+}
+
 template <class T>
 T* dalloc(zk_context* c, size_t count) {
     return static_cast<T*>(c->alloc.alloc(sizeof(T) * (count ? count : 1)));
@@ -271,6 +296,22 @@ void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
     const size_t smem = pipe_smem_bytes(v, 0);
     ZK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_spmv<<<pipe_grid(A), kPipeThreads, smem, c->stream>>>(v, x, y);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+}
+
+void spmv_dot_device(zk_context* c, const zk_csr* A, const double2* x, double2* y, const double2* w, bool conj,
+                     double2* result) {
+    const size_t extra = RedSmem<1, 0>::kBytes;
+    SellView v = sell_view(A, c, extra, 1);
+    v.sv[0] = w;
+    const size_t smem = pipe_smem_bytes(v, extra);
+    const int64_t nb = A->nblocks;
+    double* partials = static_cast<double*>(c->scratch_partials(sizeof(double2) * (nb ? nb : 1)));
+    const PlanPtrs p = c->plans_for(A->n_rows, kBlock, kComplex);
+    ZK_CUDA(cudaFuncSetAttribute(k_spmv_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_spmv_dot<<<pipe_grid(A), kRedPipeThreads, smem, c->stream>>>(
+        v, x, SpmvDotBody{y, result, c->counter, conj, c->fma != 0}, RedCfg{p, p, partials, c->counter, 0});
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }

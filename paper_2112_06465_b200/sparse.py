@@ -19,7 +19,7 @@ from . import _lib
 from .errors import DimensionError, FormatError
 from .vecops import ZVector
 
-__all__ = ["CooMatrix", "CsrMatrix", "coo_to_csr", "spmv"]
+__all__ = ["CooMatrix", "CsrMatrix", "coo_to_csr", "spmv", "spmv_dot"]
 
 
 @dataclass
@@ -191,6 +191,23 @@ def coo_to_csr(m: CooMatrix) -> CsrMatrix:
     ia = np.zeros(n_rows + 1, dtype=np.int64)
     np.cumsum(counts, out=ia[1:])
     return CsrMatrix(n_rows, n_cols, summed, ukey % n_cols, ia)
+
+
+def spmv_dot(A: CsrMatrix, x: ZVector, w: ZVector, conjugate: bool = True):
+    """``(y, <w, y>)`` with ``y = A x``, fused in one pass over the matrix:
+    bitwise ``spmv(A, x)`` then ``zdot(w, y, conjugate)`` (DEFAULT_PLAN)."""
+    from .cnum import Cplx
+    if len(x) != A.n_cols:
+        raise DimensionError(f"matrix has {A.n_cols} columns, vector has {len(x)} elements")
+    if len(w) != A.n_rows:
+        raise DimensionError(f"vector lengths differ: {len(w)} vs {A.n_rows}")
+    if A.n_rows == 0:
+        return ZVector(np.zeros(0, dtype=np.complex128)), Cplx(0.0, 0.0)
+    y = ZVector._device_new(A.n_rows)
+    out = (ctypes.c_double * 2)()
+    _lib.check(_lib.lib().zk_spmv_dotc(_lib.context(), A._device(), x._dptr(), y._dptr_out(), w._dptr(),
+                                       int(bool(conjugate)), out))
+    return y._written(), Cplx(out[0], out[1])
 
 
 def spmv(A: CsrMatrix, x: ZVector) -> ZVector:

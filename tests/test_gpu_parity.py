@@ -156,6 +156,28 @@ def test_c3_spmv_and_capped_solve_vs_oracle():
     assert bits(x.data) == bits(xo)
 
 
+@pytest.mark.parametrize("kind", ["fd", "s27", "fe"])
+def test_spmv_dot_fused_vs_oracle(kind):
+    """zk_spmv_dotc: y = A x and <w, y> in one pass == spmv then zdot, bitwise."""
+    from paper_2112_06465_b200.sparse import spmv_dot
+    if kind == "fd":
+        n, ia, ja, aa, b = problems.helmholtz_fd(3, 49, frequency=4.0, damping=0.3)
+    elif kind == "s27":
+        n, ia, ja, aa, b = problems.helmholtz_27pt(30)
+    else:
+        n, ia, ja, aa, b = problems.cylinder_p1fe(24)
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    rng = np.random.default_rng(11)
+    xv = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    wv = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y, d = spmv_dot(A, Z.ZVector(xv), Z.ZVector(wv))
+    yo = O.spmv(n, n, ia, ja, aa, xv)
+    assert bits(y.data) == bits(yo)
+    assert complex(d) == O.zdot(wv, yo)
+    y2, d2 = spmv_dot(A, Z.ZVector(xv), Z.ZVector(wv), conjugate=False)
+    assert complex(d2) == O.zdot(wv, yo, conjugate=False)
+
+
 def test_solver_host_loop_matches_graph(monkeypatch, bicgstab_golden):
     """The CUDA-graph WHILE loop and the host-driven loop are the same kernels."""
     monkeypatch.setenv("ZK_SOLVER_LOOP", "host")
