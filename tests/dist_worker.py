@@ -44,6 +44,8 @@ def solve_worker(rank, world, port, out, case, backend):
         Z.set_arithmetic(True, 262144)
         kind, cells, freq, damp, jac, guess, maxit = case
         n, ia, ja, aa, b = problems.helmholtz_fd(3, cells, frequency=freq, damping=damp)
+        if kind == "zero_rhs":
+            b = np.zeros(n, dtype=np.complex128)
         A = Z.CsrMatrix(n, n, aa, ja, ia)
         M = Z.build_jacobi(A) if jac else None
         x0 = None

@@ -35,6 +35,8 @@ def _oracle(case):
     if guess:
         rng = np.random.default_rng(7)
         x0 = rng.standard_normal(n) * 1e-3 + 0j
+    if kind == "zero_rhs":
+        b = np.zeros(n, dtype=np.complex128)
     return O.bicgstab(n, ia, ja, aa, b, minv, x0, 1e-8, maxit)
 
 
@@ -42,6 +44,7 @@ CASES = [
     ("jacobi", 33, 4.0, 0.3, True, False, 400),       # 32768 rows, 8 blocks, converges
     ("identity+guess", 33, 2.0, 0.3, False, True, 400),
     ("cap", 33, 4.0, 0.3, True, False, 5),             # stops at max_iterations
+    ("zero_rhs", 33, 4.0, 0.3, True, False, 50),       # trivial result: x = 0, history [0.0]
 ]
 
 
