@@ -278,9 +278,12 @@ class ShardedBiCGStab:
             _lib.check(lib.zk_memcpy_h2d(_lib.context(), ib.ptr, arr.ctypes.data, 8 * len(idx)))
             self._send[q] = (ib, _lib.DeviceBuffer(16 * len(idx)), len(idx))
         self.transport = NcclTransport(group) if transport == "nccl" else HostTransport(group)
-        # NCCL: replay a captured iteration (ZK_DIST_GRAPH=0 issues it op by op)
+        # NCCL: replay a captured iteration.  Verified at one rank; with peers
+        # the capture includes NCCL point-to-point ops, so it is opt-in there
+        # (ZK_DIST_GRAPH=1; =0 forces op-by-op issue everywhere).
         import os
-        self.use_graph = transport == "nccl" and os.environ.get("ZK_DIST_GRAPH", "1") != "0"
+        flag = os.environ.get("ZK_DIST_GRAPH")
+        self.use_graph = transport == "nccl" and (flag == "1" or (flag is None and self.world == 1))
         self._graph = None
 
     def __del__(self):
@@ -374,8 +377,12 @@ class ShardedBiCGStab:
             step = self._iteration
             if self.use_graph:
                 if self._graph is None:
-                    self._graph = self._capture()  # captured, not executed
-                step = self._graph.replay
+                    try:
+                        self._graph = self._capture()  # captured, not executed
+                    except Exception:  # noqa: BLE001  (capture unsupported here: issue op by op)
+                        self.use_graph = False
+                if self._graph is not None:
+                    step = self._graph.replay
             it = 0
             while True:
                 step()
