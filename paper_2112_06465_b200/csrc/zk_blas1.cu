@@ -2,9 +2,10 @@
 //
 // Elementwise kernels are HBM-bound streams: grid-stride over double2
 // (16-byte, coalesced) with 4 independent elements per thread in flight.
-// Reductions run one CTA per ReductionPlan block (zk_reduce.cuh) with the
-// ordered fold done by the last CTA, so a zdot is a single kernel launch.
+// Reductions run one CTA per ReductionPlan block (numpy's pairwise order,
+// zk_blockred.cuh) and a one-warp kernel folds the block partials in order.
 #include "zk_internal.h"
+#include "zk_blockred.cuh"
 
 namespace zk {
 
@@ -74,43 +75,55 @@ struct Norm2Op {
     __device__ void apply(int64_t, const Item& it, double (&v)[1]) const { v[0] = abs2_np(it.x); }
 };
 
-// Blocked zdot: one CTA per reduction block; the last CTA folds the partials.
-__global__ void __launch_bounds__(kRedThreads, 2) k_zdot_blocked(int64_t n, const double2* __restrict__ x,
-                                                              const double2* __restrict__ y, bool conj,
-                                                              int64_t block, PlanPtrs plans, double2* partials,
-                                                              unsigned int* counter, double2* result, bool fma) {
-    extern __shared__ double2 smem_c[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
-    double2 out[1];
-    block_reduce<double2, 1>(plans, n, block, blockIdx.x, DotOp{x, y, conj, fma}, smem_c, out);
-    if (threadIdx.x == 0) partials[blockIdx.x] = out[0];
-    if (arrive_last(counter, gridDim.x, &s_flag)) {
-        double2 tot;
-        ordered_fold<double2>(partials, 1, gridDim.x, smem_c, 2048, &tot, s_res);
-        if (threadIdx.x == 0) {
-            *result = tot;
-            *counter = 0;
-        }
+// Block partials, one CTA per reduction block and a single barrier: every
+// thread runs its (leaf, lane) items, then warp 0 alone combines the tree
+// (__syncwarp only) and stores the partial while the other warps exit.  No
+// arrival counter: a one-warp kernel folds the partials afterwards (a
+// per-CTA fence + same-address atomic cost ~20% of the pass, measured).
+template <typename V, class Op>
+__device__ __forceinline__ void block_partial(PlanPtrs plans, int64_t n, int64_t block, const Op& op, V* nodes,
+                                              V* partials) {
+    const int64_t blk = blockIdx.x;
+    const int64_t base = blk * block;
+    const char* plan = (base + block <= n) ? plans.full : plans.tail;
+    V v0[1];
+    if (threadIdx.x == 0) {
+        typename Op::Item it = op.load(base);
+        op.apply(base, it, v0);
     }
+    leaf_phase<V, 1>(plan, base + 1, op, nodes, blockDim.x);
+    __syncthreads();
+    if ((threadIdx.x >> 5) != 0) return;
+    V pw[1];
+    warp_tree<V, 1>(plan, nodes, pw);
+    if ((threadIdx.x & 31) == 0) partials[blk] = plan_hdr(plan)->L > 0 ? VT<V>::add(v0[0], pw[0]) : v0[0];
 }
 
-__global__ void __launch_bounds__(kRedThreads, 3) k_znorm2_blocked(int64_t n, const double2* __restrict__ x,
-                                                                int64_t block, PlanPtrs plans, double* partials,
-                                                                unsigned int* counter, double* result) {
-    extern __shared__ double smem_r[];
-    __shared__ unsigned int s_flag;
-    __shared__ double s_res[16];
-    double out[1];
-    block_reduce<double, 1>(plans, n, block, blockIdx.x, Norm2Op{x}, smem_r, out);
-    if (threadIdx.x == 0) partials[blockIdx.x] = out[0];
-    if (arrive_last(counter, gridDim.x, &s_flag)) {
-        double tot;
-        ordered_fold<double>(partials, 1, gridDim.x, smem_r, 4096, &tot, s_res);
-        if (threadIdx.x == 0) {
-            *result = __dsqrt_rn(tot);
-            *counter = 0;
+__global__ void __launch_bounds__(kRedThreads, 2) k_zdot_partials(int64_t n, const double2* __restrict__ x,
+                                                                const double2* __restrict__ y, bool conj,
+                                                                int64_t block, PlanPtrs plans, double2* partials,
+                                                                bool fma) {
+    extern __shared__ double2 nodes_c[];
+    block_partial<double2>(plans, n, block, DotOp{x, y, conj, fma}, nodes_c, partials);
+}
+
+__global__ void __launch_bounds__(kRedThreads, 3) k_znorm2_partials(int64_t n, const double2* __restrict__ x,
+                                                                  int64_t block, PlanPtrs plans, double* partials) {
+    extern __shared__ double nodes_r[];
+    block_partial<double>(plans, n, block, Norm2Op{x}, nodes_r, partials);
+}
+
+// Left fold of the block partials (vecops.py:159-161), one warp.
+template <typename V>
+__global__ void __launch_bounds__(32) k_fold(const V* partials, int64_t nb, V* result, bool sqrt_result) {
+    __shared__ double scratch[2048];
+    V tot;
+    warp_fold<V>(partials, 1, nb, reinterpret_cast<V*>(scratch), (int)(2048 * sizeof(double) / sizeof(V)), &tot);
+    if (threadIdx.x == 0) {
+        if constexpr (sizeof(V) == sizeof(double)) {
+            if (sqrt_result) tot = __dsqrt_rn(tot);
         }
+        *result = tot;
     }
 }
 
@@ -135,13 +148,6 @@ __global__ void k_znorm2_seq(int64_t n, const double2* __restrict__ x, double* r
 }
 
 }  // namespace
-
-// Shared-memory bytes for the block pass + fold of a plan pair.
-size_t reduce_smem_bytes(int nnodes, int nacc, size_t vbytes, int64_t fold_chunk) {
-    size_t a = (size_t)nnodes * nacc * vbytes;
-    size_t b = (size_t)fold_chunk * nacc * vbytes;
-    return a > b ? a : b;
-}
 
 void launch_zscal(zk_context* c, int64_t n, double2 a, double2* x) {
     if (n <= 0) return;
@@ -187,14 +193,15 @@ void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, b
     int tail = (int32_t)(n - (nb - 1) * block) - 1;
     int nn2 = plan_nnodes(c, tail, kComplex);
     if (nn2 > nnodes) nnodes = nn2;
-    size_t smem = reduce_smem_bytes(nnodes, 1, sizeof(double2), 2048);
+    const size_t smem = (size_t)nnodes * sizeof(double2);
     double2* partials = static_cast<double2*>(c->scratch_partials(sizeof(double2) * nb));
     if (smem > 48 * 1024)
-        ZK_CUDA(cudaFuncSetAttribute(k_zdot_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_zdot_blocked<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, x, y, conj, block, p, partials, c->counter,
-                                                                 result, c->fma);
+        ZK_CUDA(cudaFuncSetAttribute(k_zdot_partials, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_zdot_partials<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, x, y, conj, block, p, partials, c->fma);
     ZK_CUDA(cudaGetLastError());
-    c->launches++;
+    k_fold<double2><<<1, 32, 0, c->stream>>>(partials, nb, result, false);
+    ZK_CUDA(cudaGetLastError());
+    c->launches += 2;
 }
 
 void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result) {
@@ -210,13 +217,15 @@ void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, in
     int tail = (int32_t)(n - (nb - 1) * block) - 1;
     int nn2 = plan_nnodes(c, tail, kReal);
     if (nn2 > nnodes) nnodes = nn2;
-    size_t smem = reduce_smem_bytes(nnodes, 1, sizeof(double), 4096);
+    const size_t smem = (size_t)nnodes * sizeof(double);
     double* partials = static_cast<double*>(c->scratch_partials(sizeof(double) * nb));
     if (smem > 48 * 1024)
-        ZK_CUDA(cudaFuncSetAttribute(k_znorm2_blocked, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_znorm2_blocked<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, x, block, p, partials, c->counter, result);
+        ZK_CUDA(cudaFuncSetAttribute(k_znorm2_partials, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_znorm2_partials<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, x, block, p, partials);
     ZK_CUDA(cudaGetLastError());
-    c->launches++;
+    k_fold<double><<<1, 32, 0, c->stream>>>(partials, nb, result, true);
+    ZK_CUDA(cudaGetLastError());
+    c->launches += 2;
 }
 
 }  // namespace zk

@@ -80,16 +80,4 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-// Barrier policies for the block-reduction helpers.
-struct CtaSync {
-    __device__ __forceinline__ void operator()() const { __syncthreads(); }
-    __device__ __forceinline__ int nthreads() const { return blockDim.x; }
-};
-
-template <int N>
-struct GroupSync {  // the first N threads of the CTA (consumer warps), barrier 1
-    __device__ __forceinline__ void operator()() const { named_sync(1, N); }
-    __device__ __forceinline__ int nthreads() const { return N; }
-};
-
 }  // namespace zk
