@@ -55,7 +55,7 @@ struct SolverBufs {
     SolverState* st;
     int64_t n, nblocks;
     bool jacobi, fma;
-    int dist;          // row-sharded solve: block partials are folded across ranks (k_dist_finish)
+    int dist;          // row-sharded solve: block partials are folded across ranks (k_fold_finish)
 };
 
 constexpr int kNodesPerBuf = 2 * 136;             // node slots per buffer (<= 129 nodes x NACC 2)
@@ -300,9 +300,13 @@ __global__ void __launch_bounds__(kRedPipeThreads, 1) k_true_res(SellView A, Sol
 // One CTA loops over blocks; per block: leaf phase (all threads, operands
 // prefetched in registers), one CTA barrier, then warp 0 combines the tree
 // while the other warps start the next block.  Nodes are double-buffered.
-template <typename V, int NACC, class Op, class Done>
+// The block partials are only stored here: k_fold_finish (one warp, launched
+// after the pass) folds them in order and runs the scalar recurrences -- a
+// per-block fence + arrival atomic in warp 0 would stall the next block's
+// barrier (measured ~20% of a standalone reduction pass).
+template <typename V, int NACC, class Op>
 __device__ __forceinline__ void persistent_blocks(PlanPtrs plans, int64_t n, int64_t nblocks, const Op& op,
-                                                  V* nodes, V* partials, unsigned int* counter, Done& done) {
+                                                  V* nodes, V* partials) {
     int buf = 0;
     for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
         const int64_t base = blk * kBlock;
@@ -319,7 +323,11 @@ __device__ __forceinline__ void persistent_blocks(PlanPtrs plans, int64_t n, int
         if ((threadIdx.x >> 5) != 0) continue;
         V pw[NACC];
         warp_tree<V, NACC>(plan, nb, pw);
-        if (warp_finish<V, NACC>(plan, v0, pw, partials, blk, counter, (unsigned)nblocks)) done();
+        if ((threadIdx.x & 31) == 0) {
+            const bool has = plan_hdr(plan)->L > 0;
+#pragma unroll
+            for (int a = 0; a < NACC; ++a) partials[blk * NACC + a] = has ? VT<V>::add(v0[a], pw[a]) : v0[a];
+        }
     }
 }
 
@@ -366,17 +374,8 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanP
     if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;  // loop-body executions (launch accounting)
     if (st->done) return;
     SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
-    double* nodes = reinterpret_cast<double*>(smem + kFoldScratch);
-    auto done = [&]() {
-        if (B.dist) {
-            if ((threadIdx.x & 31) == 0) st->counter = 0;
-            return;
-        }
-        double ss;
-        warp_fold<double>(B.partials, 1, B.nblocks, reinterpret_cast<double*>(smem), kFoldScratch / 8, &ss);
-        if ((threadIdx.x & 31) == 0) SUpdFinish{B}.finish(&ss);
-    };
-    persistent_blocks<double, 1>(pr, B.n, B.nblocks, op, nodes, B.partials, &st->counter, done);
+    persistent_blocks<double, 1>(pr, B.n, B.nblocks, op, reinterpret_cast<double*>(smem + kFoldScratch),
+                                 B.partials);
 }
 
 // ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
@@ -447,32 +446,23 @@ __global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, Plan
     if (st->done) return;
     const double2 a = st->alpha, w = st->omega;
     XrOp op{B.x, B.r, B.ph, B.sh, B.s, B.t, B.rs, a, w, neg(w), st->alpha_applied != 0, B.fma};
-    double2* nodes = reinterpret_cast<double2*>(smem + kFoldScratch);
-    double2* PC = reinterpret_cast<double2*>(B.partials);
-    auto done = [&]() {
-        if (B.dist) {
-            if ((threadIdx.x & 31) == 0) st->counter = 0;
-            return;
-        }
-        double2 rho_next;
-        warp_fold<double2>(PC, 1, B.nblocks, reinterpret_cast<double2*>(smem), kFoldScratch / 16, &rho_next);
-        if ((threadIdx.x & 31) == 0) XrFinish{B}.finish(reinterpret_cast<const double*>(&rho_next));
-    };
-    persistent_blocks<double2, 1>(pc, B.n, B.nblocks, op, nodes, PC, &st->counter, done);
+    persistent_blocks<double2, 1>(pc, B.n, B.nblocks, op, reinterpret_cast<double2*>(smem + kFoldScratch),
+                                  reinterpret_cast<double2*>(B.partials));
 }
 
-// ---- row-sharded solve: cross-rank fold of the block partials -----------------
-// `gathered` holds every rank's block partials (rank r at r*maxb*NP, its
-// counts[r] blocks first), i.e. the global block order of the unsharded
-// vector (rank row ranges are 4096-aligned), so one warp folding them in
-// that order reproduces vecops.py:159-161 exactly, on every rank.
+// ---- ordered fold of block partials + the phase's scalar recurrences ----------
+// `gathered` holds the block partials of every rank (rank r at r*maxb*NP, its
+// counts[r] blocks first) -- one rank for the 1-GPU level-1 phases, all
+// ranks (all-gathered) for the row-sharded solve.  That is the global block
+// order of the unsharded vector (rank row ranges are 4096-aligned), so one
+// warp folding them in order reproduces vecops.py:159-161 exactly.
 constexpr int kMaxRanks = 64;
 struct RankCounts {
     int64_t n[kMaxRanks];
 };
 
 template <class Fin>
-__global__ void __launch_bounds__(32) k_dist_finish(Fin fin, const double* __restrict__ gathered, int nranks,
+__global__ void __launch_bounds__(32) k_fold_finish(Fin fin, const double* __restrict__ gathered, int nranks,
                                                     int64_t maxb, RankCounts counts, int phase_gate) {
     __shared__ double scratch[4 * 512];
     const SolverState* st = fin.B.st;
@@ -510,6 +500,7 @@ struct Launch {
     RedCfg red;
     PlanPtrs pc, pr;
     unsigned nb, ew, pg, rg;  // blocks, elementwise grid, SpMV grid, level-1 persistent grid
+    RankCounts one;           // {nblocks}: the 1-GPU fold's partial count
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
@@ -539,6 +530,7 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
                  PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(3, s);
     k_s_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
+    k_fold_finish<<<1, 32, 0, s>>>(SUpdFinish{L.P->bufs}, L.P->bufs.partials, 1, L.nb, L.one, 0);
     if (pe) pe->rec(4, s);
     k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(5, s);
@@ -547,6 +539,7 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.red);
     if (pe) pe->rec(7, s);
     k_xr_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
+    k_fold_finish<<<1, 32, 0, s>>>(XrFinish{L.P->bufs}, L.P->bufs.partials, 1, L.nb, L.one, 0);
     if (pe) pe->rec(8, s);
     k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
     if (pe) pe->rec(9, s);
@@ -555,7 +548,8 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.red, cond, use_cond);
     if (pe) pe->rec(11, s);
 }
-constexpr int kBodyKernels = 8;
+constexpr int kBodyKernels = 10;  // launches per loop trip
+constexpr int kBodyPhases = 8;    // timed phases per loop trip (ev[3..11])
 
 void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
     ZK_CUDA(cudaEventSynchronize(pe.ev[last + 1]));
@@ -687,6 +681,8 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.pr = c->plans_for(n, kBlock, kReal);
     L.red = RedCfg{L.pc, L.pr, B.partials, &B.st->counter, B.dist};
     L.nb = (unsigned)B.nblocks;
+    L.one = RankCounts{};
+    L.one.n[0] = B.nblocks;
     L.pg = pipe_grid(A);
     L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
     int64_t ewg = (n + 255) / 256;
@@ -745,7 +741,7 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
             ZK_CUDA(cudaGetLastError());
             ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
             ZK_CUDA(cudaStreamSynchronize(s));
-            if (pe.on) accumulate(c, pe, kPrologueKernels, kPrologueKernels + kBodyKernels - 1);
+            if (pe.on) accumulate(c, pe, kPrologueKernels, kPrologueKernels + kBodyPhases - 1);
             if (out.done) break;
         }
         if (pe.on)
@@ -894,13 +890,13 @@ void dist_finish(DistSolver* D, int phase, const int64_t* rank_blocks) {
     const int nr = D->nranks;
     const int64_t mb = D->maxb;
     switch (phase) {
-        case ZK_DPHASE_SETUP: k_dist_finish<<<1, 32, 0, s>>>(SetupBody{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_PIVOT: k_dist_finish<<<1, 32, 0, s>>>(PivotBody{B, 0, 0}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_S_UPDATE: k_dist_finish<<<1, 32, 0, s>>>(SUpdFinish{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_TRUE_RES_S: k_dist_finish<<<1, 32, 0, s>>>(ResBody<0>{B}, g, nr, mb, rc, 1); break;
-        case ZK_DPHASE_SPMV_T: k_dist_finish<<<1, 32, 0, s>>>(TBody{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_XR_UPDATE: k_dist_finish<<<1, 32, 0, s>>>(XrFinish{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_TRUE_RES: k_dist_finish<<<1, 32, 0, s>>>(ResBody<1>{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_SETUP: k_fold_finish<<<1, 32, 0, s>>>(SetupBody{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_PIVOT: k_fold_finish<<<1, 32, 0, s>>>(PivotBody{B, 0, 0}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_S_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(SUpdFinish{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_TRUE_RES_S: k_fold_finish<<<1, 32, 0, s>>>(ResBody<0>{B}, g, nr, mb, rc, 1); break;
+        case ZK_DPHASE_SPMV_T: k_fold_finish<<<1, 32, 0, s>>>(TBody{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_XR_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(XrFinish{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_TRUE_RES: k_fold_finish<<<1, 32, 0, s>>>(ResBody<1>{B}, g, nr, mb, rc, 0); break;
         default: throw ZkError{ZK_ERR_PARAMETER, "phase has no reduction"};
     }
     ZK_CUDA(cudaGetLastError());
