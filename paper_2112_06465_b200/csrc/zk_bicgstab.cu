@@ -51,6 +51,7 @@ struct SolverState {
 struct SolverBufs {
     double2 *x, *b, *minv, *r, *rs, *p, *v, *s, *t, *ph, *sh;
     double* partials;  // nblocks * 4 doubles
+    double* slots;     // nblocks * 4 doubles at kSlotEmpty between passes (1-GPU streaming fold)
     double* hist;      // hist_cap doubles
     SolverState* st;
     int64_t n, nblocks;
@@ -61,8 +62,7 @@ struct SolverBufs {
 constexpr int kNodesPerBuf = 2 * 136;             // node slots per buffer (<= 129 nodes x NACC 2)
 constexpr int kNodeBytes = 2 * kNodesPerBuf * 16;  // double-buffered plan nodes
 constexpr int kRedThreads = 288;                   // 65 complex leaves x 4 lanes fit one pass
-constexpr int kFoldScratch = 8 * 1024;             // warp_fold staging in the level-1 kernels
-constexpr int kEwSmem = kFoldScratch + kNodeBytes;
+constexpr int kEwSmem = kNodeBytes;
 
 struct SolverPlan {
     int64_t n = 0;
@@ -296,19 +296,47 @@ __global__ void __launch_bounds__(kRedPipeThreads, 1) k_true_res(SellView A, Sol
     sell_run<1>(A, B.x, nullptr, body, R, smem);
 }
 
+__global__ void k_fill_empty(double* p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = __longlong_as_double((long long)kSlotEmpty);
+}
+
 // ---- persistent block-pass kernels for the fused level-1 phases ----------
 // One CTA loops over blocks; per block: leaf phase (all threads, operands
 // prefetched in registers), one CTA barrier, then warp 0 combines the tree
 // while the other warps start the next block.  Nodes are double-buffered.
-// The block partials are only stored here: k_fold_finish (one warp, launched
-// after the pass) folds them in order and runs the scalar recurrences -- a
-// per-block fence + arrival atomic in warp 0 would stall the next block's
-// barrier (measured ~20% of a standalone reduction pass).
-template <typename V, int NACC, class Op>
+// STREAM (1 GPU): CTA 0 is the folder -- its warp 0 folds the partials in
+// block order while CTAs 1.. produce them (stream_fold, no per-block fence
+// or atomic) and runs the phase's scalar recurrences (fin.finish), so the
+// serial fold (~17 cycles per partial) overlaps the pass instead of
+// following it.  !STREAM (row-sharded solve): the partials are stored for
+// the cross-rank gather and k_fold_finish folds them in global order.
+// The folder warp's work, out of line so it does not add to the workers'
+// register allocation.
+template <int NP, class Fin>
+__device__ __noinline__ void fold_and_finish(double* slots, int64_t nblocks, Fin fin) {
+    double t[NP];
+    stream_fold<NP>(slots, nblocks, t);
+    if (threadIdx.x == 0) fin.finish(t);
+}
+
+template <bool STREAM, typename V, int NACC, class Op, class Fin>
 __device__ __forceinline__ void persistent_blocks(PlanPtrs plans, int64_t n, int64_t nblocks, const Op& op,
-                                                  V* nodes, V* partials) {
+                                                  V* nodes, double* partials, double* slots, Fin fin) {
+    constexpr int NP = NACC * (int)(sizeof(V) / sizeof(double));
+    static_assert(NP == Fin::kNP, "partials per block");
+    int64_t first = blockIdx.x, stride = gridDim.x;
+    if constexpr (STREAM) {
+        if (blockIdx.x == 0) {
+            if (threadIdx.x < 32) fold_and_finish<NP>(slots, nblocks, fin);
+            return;
+        }
+        first -= 1;
+        stride -= 1;
+    }
+    double* out = STREAM ? slots : partials;
     int buf = 0;
-    for (int64_t blk = blockIdx.x; blk < nblocks; blk += gridDim.x) {
+    for (int64_t blk = first; blk < nblocks; blk += stride) {
         const int64_t base = blk * kBlock;
         const char* plan = (base + kBlock <= n) ? plans.full : plans.tail;
         V* nb = nodes + buf * kNodesPerBuf;
@@ -326,7 +354,15 @@ __device__ __forceinline__ void persistent_blocks(PlanPtrs plans, int64_t n, int
         if ((threadIdx.x & 31) == 0) {
             const bool has = plan_hdr(plan)->L > 0;
 #pragma unroll
-            for (int a = 0; a < NACC; ++a) partials[blk * NACC + a] = has ? VT<V>::add(v0[a], pw[a]) : v0[a];
+            for (int a = 0; a < NACC; ++a) {
+                const V p = has ? VT<V>::add(v0[a], pw[a]) : v0[a];
+                const double* pd = reinterpret_cast<const double*>(&p);
+#pragma unroll
+                for (int c = 0; c < NP / NACC; ++c) {
+                    if constexpr (STREAM) slot_store(out + (blk * NACC + a) * (NP / NACC) + c, pd[c]);
+                    else out[(blk * NACC + a) * (NP / NACC) + c] = pd[c];
+                }
+            }
         }
     }
 }
@@ -368,14 +404,15 @@ struct SUpdFinish {
     }
 };
 
+template <bool STREAM>
 __global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;  // loop-body executions (launch accounting)
     if (st->done) return;
     SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
-    persistent_blocks<double, 1>(pr, B.n, B.nblocks, op, reinterpret_cast<double*>(smem + kFoldScratch),
-                                 B.partials);
+    persistent_blocks<STREAM, double, 1>(pr, B.n, B.nblocks, op, reinterpret_cast<double*>(smem), B.partials,
+                                         B.slots, SUpdFinish{B});
 }
 
 // ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
@@ -440,14 +477,15 @@ struct XrFinish {
     }
 };
 
+template <bool STREAM>
 __global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, PlanPtrs pc) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
     if (st->done) return;
     const double2 a = st->alpha, w = st->omega;
     XrOp op{B.x, B.r, B.ph, B.sh, B.s, B.t, B.rs, a, w, neg(w), st->alpha_applied != 0, B.fma};
-    persistent_blocks<double2, 1>(pc, B.n, B.nblocks, op, reinterpret_cast<double2*>(smem + kFoldScratch),
-                                  reinterpret_cast<double2*>(B.partials));
+    persistent_blocks<STREAM, double2, 1>(pc, B.n, B.nblocks, op, reinterpret_cast<double2*>(smem), B.partials,
+                                          B.slots, XrFinish{B});
 }
 
 // ---- ordered fold of block partials + the phase's scalar recurrences ----------
@@ -464,7 +502,7 @@ struct RankCounts {
 template <class Fin>
 __global__ void __launch_bounds__(32) k_fold_finish(Fin fin, const double* __restrict__ gathered, int nranks,
                                                     int64_t maxb, RankCounts counts, int phase_gate) {
-    __shared__ double scratch[4 * 512];
+    __shared__ double scratch[2 * kFoldStage];
     const SolverState* st = fin.B.st;
     if (st->done || (phase_gate == 1 && !st->scheck)) return;
     constexpr int NP = Fin::kNP;
@@ -472,7 +510,7 @@ __global__ void __launch_bounds__(32) k_fold_finish(Fin fin, const double* __res
     bool first = true;
     for (int r = 0; r < nranks; ++r) {
         if (counts.n[r] <= 0) continue;
-        warp_fold_cont(gathered + (int64_t)r * maxb * NP, NP, counts.n[r], scratch, 512, tot, first);
+        warp_fold_cont(gathered + (int64_t)r * maxb * NP, NP, counts.n[r], scratch, tot, first);
         first = false;
     }
     double t[NP];
@@ -500,6 +538,7 @@ struct Launch {
     RedCfg red;
     PlanPtrs pc, pr;
     unsigned nb, ew, pg, rg;  // blocks, elementwise grid, SpMV grid, level-1 persistent grid
+    unsigned rs;              // streaming level-1 grid: folder CTA + workers
     RankCounts one;           // {nblocks}: the 1-GPU fold's partial count
 };
 
@@ -529,8 +568,7 @@ constexpr int kPrologueKernels = 3;
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(3, s);
-    k_s_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
-    k_fold_finish<<<1, 32, 0, s>>>(SUpdFinish{L.P->bufs}, L.P->bufs.partials, 1, L.nb, L.one, 0);
+    k_s_update<true><<<L.rs, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
     if (pe) pe->rec(4, s);
     k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(5, s);
@@ -538,8 +576,7 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     if (pe) pe->rec(6, s);
     k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.red);
     if (pe) pe->rec(7, s);
-    k_xr_update<<<L.rg, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
-    k_fold_finish<<<1, 32, 0, s>>>(XrFinish{L.P->bufs}, L.P->bufs.partials, 1, L.nb, L.one, 0);
+    k_xr_update<true><<<L.rs, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
     if (pe) pe->rec(8, s);
     k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
     if (pe) pe->rec(9, s);
@@ -548,7 +585,7 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.red, cond, use_cond);
     if (pe) pe->rec(11, s);
 }
-constexpr int kBodyKernels = 10;  // launches per loop trip
+constexpr int kBodyKernels = 8;   // launches per loop trip
 constexpr int kBodyPhases = 8;    // timed phases per loop trip (ev[3..11])
 
 void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
@@ -567,8 +604,10 @@ void set_attrs(const Launch& L) {
     smem_attr(k_spmv_t, L.smem_t);
     smem_attr(k_true_res<0>, L.smem_r);
     smem_attr(k_true_res<1>, L.smem_r);
-    smem_attr(k_s_update, kEwSmem);
-    smem_attr(k_xr_update, kEwSmem);
+    smem_attr(k_s_update<true>, kEwSmem);
+    smem_attr(k_xr_update<true>, kEwSmem);
+    smem_attr(k_s_update<false>, kEwSmem);
+    smem_attr(k_xr_update<false>, kEwSmem);
 }
 
 bool use_graph() {
@@ -615,7 +654,7 @@ void destroy_solver_plan(zk_context* c, SolverPlan* P) {
     if (P->exec) cudaGraphExecDestroy(P->exec);
     if (P->graph) cudaGraphDestroy(P->graph);
     SolverBufs& B = P->bufs;
-    void* ptrs[] = {B.x, B.b, B.minv, B.r, B.rs, B.p, B.v, B.s, B.t, B.partials, B.hist, B.st};
+    void* ptrs[] = {B.x, B.b, B.minv, B.r, B.rs, B.p, B.v, B.s, B.t, B.partials, B.slots, B.hist, B.st};
     for (void* p : ptrs)
         if (p) c->alloc.free(p);
     if (B.jacobi) {
@@ -649,6 +688,9 @@ static SolverPlan* get_plan(zk_context* c, zk_csr* A, bool jacobi, int64_t maxit
     B.ph = jacobi ? vec() : B.p;   // identity: M.apply is a copy, bitwise equal
     B.sh = jacobi ? vec() : B.s;
     B.partials = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)(B.nblocks ? B.nblocks : 1)));
+    B.slots = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)(B.nblocks ? B.nblocks : 1)));
+    k_fill_empty<<<64, 256, 0, c->stream>>>(B.slots, 4 * (B.nblocks ? B.nblocks : 1));
+    ZK_CUDA(cudaGetLastError());
     B.hist = static_cast<double*>(c->alloc.alloc(sizeof(double) * P->hist_cap));
     B.st = static_cast<SolverState*>(c->alloc.alloc(sizeof(SolverState)));
     slot = P;
@@ -679,12 +721,13 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
-    L.red = RedCfg{L.pc, L.pr, B.partials, &B.st->counter, B.dist};
+    L.red = RedCfg{L.pc, L.pr, B.partials, &B.st->counter, B.dist, B.dist ? nullptr : B.slots};
     L.nb = (unsigned)B.nblocks;
     L.one = RankCounts{};
     L.one.n[0] = B.nblocks;
     L.pg = pipe_grid(A);
     L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
+    L.rs = 1 + (unsigned)(B.nblocks < 2 * num_sms() - 1 ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms() - 1);
     int64_t ewg = (n + 255) / 256;
     int64_t cap = (int64_t)num_sms() * 8;
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
@@ -867,11 +910,11 @@ void dist_phase(DistSolver* D, int phase) {
         case ZK_DPHASE_SETUP: k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); break;
         case ZK_DPHASE_P_FIRST: k_p_first<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_PIVOT: k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, B, L.red, 0, 0); break;
-        case ZK_DPHASE_S_UPDATE: k_s_update<<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pr); break;
+        case ZK_DPHASE_S_UPDATE: k_s_update<false><<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pr); break;
         case ZK_DPHASE_X_ALPHA: k_x_alpha<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_TRUE_RES_S: k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_SPMV_T: k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, B, L.red); break;
-        case ZK_DPHASE_XR_UPDATE: k_xr_update<<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pc); break;
+        case ZK_DPHASE_XR_UPDATE: k_xr_update<false><<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pc); break;
         case ZK_DPHASE_TRUE_RES: k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_P_NEXT: k_p_next<<<L.ew, 256, 0, s>>>(B); break;
         default: throw ZkError{ZK_ERR_PARAMETER, "unknown solver phase"};

@@ -239,61 +239,246 @@ __device__ __forceinline__ bool warp_finish(const char* plan, const V (&v0)[NACC
     return last != 0;
 }
 
+// Ordered fold core.  partials holds nb rows of nchains doubles; lane c
+// (< nchains) adds column c to `tot` in row order (__dadd_rn: the Python
+// left fold, one rounding per add).  The serial add chain is the critical
+// path, so nothing else may sit on it: the warp stages kFoldStage doubles
+// at a time into a double-buffered smem window (scratch: 2*kFoldStage
+// doubles) with the next window's __ldcg loads issued before the current
+// window is folded, and each chain lane reads 16 values into registers
+// ahead of its 16 dependent adds (an LDS per add left the smem latency on
+// the chain: ~19 cycles per partial, measured).
+constexpr int kFoldStage = 512;
+
+__device__ __forceinline__ void fold_stream(const double* partials, int nchains, int64_t nb, double* scratch,
+                                            double& tot) {
+    constexpr int PER = kFoldStage / 32;
+    const int lane = threadIdx.x & 31;
+    const int64_t total = nb * nchains;
+    double r[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int64_t i = (int64_t)k * 32 + lane;
+        r[k] = i < total ? __ldcg(partials + i) : 0.0;
+    }
+    int stage = 0;
+    for (int64_t e0 = 0; e0 < total; e0 += kFoldStage, stage ^= 1) {
+        double* buf = scratch + stage * kFoldStage;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) buf[k * 32 + lane] = r[k];
+        __syncwarp();
+        const int64_t e1 = (total - e0 < kFoldStage) ? total : e0 + kFoldStage;
+        if (e1 < total) {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int64_t i = e1 + (int64_t)k * 32 + lane;
+                r[k] = i < total ? __ldcg(partials + i) : 0.0;
+            }
+        }
+        if (lane < nchains) {
+            int j = (int)(((int64_t)lane - e0 % nchains + nchains) % nchains);  // first index of chain in window
+            const int n = (int)(e1 - e0);
+            for (; j + 15 * nchains < n; j += 16 * nchains) {
+                double v[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] = buf[j + k * nchains];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) tot = __dadd_rn(tot, v[k]);
+            }
+            for (; j < n; j += nchains) tot = __dadd_rn(tot, buf[j]);
+        }
+    }
+    __syncwarp();
+}
+
 // Ordered fold of chains continued across calls: lane c (< nchains) adds
 // partials[b*nchains + c] for b < nb to its running total `tot` (first
-// call: first = true starts the chain at partials[c]).  Whole warp.
+// call: first = true starts the chain; -0.0 + p == p for every p, so
+// starting from -0.0 is the left fold that starts at partials[c]).
 __device__ __forceinline__ void warp_fold_cont(const double* partials, int nchains, int64_t nb, double* scratch,
-                                               int chunk, double& tot, bool first) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t c0 = 0; c0 < nb; c0 += chunk) {
-        const int64_t cn = (nb - c0 < chunk) ? nb - c0 : chunk;
-        for (int64_t i = lane; i < cn * nchains; i += 32) scratch[i] = __ldcg(partials + c0 * nchains + i);
-        __syncwarp();
-        if (lane < nchains) {
-            int64_t b = 0;
-            if (first && c0 == 0) {
-                tot = scratch[lane];
-                b = 1;
-            }
-#pragma unroll 16
-            for (; b < cn; ++b) tot = __dadd_rn(tot, scratch[b * nchains + lane]);
-        }
-        __syncwarp();
-    }
+                                               double& tot, bool first) {
+    if (first) tot = -0.0;
+    fold_stream(partials, nchains, nb, scratch, tot);
 }
 
 // Ordered fold by one warp (vecops.py:159-161): lane c (< nacc*NC) folds the
-// real component chain c; partials are staged through `scratch` (chunk*nacc
-// values).  Result (nacc values) valid in lane 0.
+// real component chain c.  scratch: 2*kFoldStage doubles.  Result (nacc
+// values) valid in lane 0.
 template <typename V>
-__device__ __forceinline__ void warp_fold(const V* partials, int nacc, int64_t nb, V* scratch, int chunk, V* result) {
+__device__ __forceinline__ void warp_fold(const V* partials, int nacc, int64_t nb, V* scratch, V* result) {
     constexpr int NC = sizeof(V) / sizeof(double);
     const int lane = threadIdx.x & 31;
     const int nchains = nacc * NC;
-    const int a = lane / NC, comp = lane % NC;
-    const double* sd = reinterpret_cast<const double*>(scratch);
-    double tot = 0.0;
-    for (int64_t c0 = 0; c0 < nb; c0 += chunk) {
-        const int64_t cn = (nb - c0 < chunk) ? nb - c0 : chunk;
-        const int64_t nv = cn * nacc;
-        for (int64_t i = lane; i < nv; i += 32) scratch[i] = __ldcg(partials + c0 * nacc + i);
-        __syncwarp();
-        if (lane < nchains) {
-            int64_t b = 0;
-            if (c0 == 0) {
-                tot = sd[a * NC + comp];
-                b = 1;
-            }
-#pragma unroll 16
-            for (; b < cn; ++b) tot = __dadd_rn(tot, sd[(b * nacc + a) * NC + comp]);
-        }
-        __syncwarp();
-    }
+    double tot = -0.0;
+    fold_stream(reinterpret_cast<const double*>(partials), nchains, nb, reinterpret_cast<double*>(scratch), tot);
     double* r = reinterpret_cast<double*>(result);
     for (int c = 0; c < nchains; ++c) {
         const double v = __shfl_sync(0xffffffffu, tot, c);
         if (lane == 0) r[c] = v;
     }
+}
+
+// ---- streaming ordered fold ---------------------------------------------------
+// Block partials published into slots that hold kSlotEmpty (a signalling
+// NaN: arithmetic never produces one, NaN results are quiet) until their
+// value lands; one warp folds them in block order while the pass is still
+// running and re-marks each consumed slot empty for the next pass.  No
+// fence or atomic per block: each slot is its own flag.
+constexpr unsigned long long kSlotEmpty = 0x7FF47FF47FF47FF4ull;
+constexpr int kPollPer = 16;  // slots per lane in flight per poll round
+
+__device__ __forceinline__ void slot_store(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double slot_load(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// tot += buf[j0 + m*NCH] for m < cnt in order, the smem loads of the next
+// 16 issued ahead of the current 16 dependent adds (the chain stays pure
+// DADD, ~14 cycles per add on B200).
+template <int NCH>
+__device__ __forceinline__ double chain_fold(double tot, const double* buf, int j0, int cnt) {
+    const double* q = buf + j0;
+    int m = 0;
+    if (cnt >= 16) {
+        double w[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) w[k] = q[k * NCH];
+        for (; m + 32 <= cnt; m += 16) {
+            double u[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) u[k] = q[(m + 16 + k) * NCH];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) tot = __dadd_rn(tot, w[k]);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) w[k] = u[k];
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) tot = __dadd_rn(tot, w[k]);
+        m += 16;
+    }
+    for (; m < cnt; ++m) tot = __dadd_rn(tot, q[m * NCH]);
+    return tot;
+}
+
+// Fold nrows*NCH slots in row order, lane c < NCH carrying chain c (column
+// c); result[0..NCH) valid in lane 0.  Whole warp.  Per round the warp
+// polls 32*kPollPer slots with all loads in flight, waits for the missing
+// ones, re-marks them empty and stages them in smem; the next round's loads
+// are issued before this round is folded, so the poll's L2 round trip
+// overlaps the add chain (the chain starts from -0.0: -0.0 + p == p, the
+// left fold starting at the first partial).
+template <int NCH>
+__device__ __forceinline__ void stream_fold(double* slots, int64_t nrows, double* result) {
+    constexpr int W = 32 * kPollPer;
+    __shared__ double sbuf[2 * W];
+    const int lane = threadIdx.x & 31;
+    const int64_t total = nrows * NCH;
+    const double empty = __longlong_as_double((long long)kSlotEmpty);
+    double tot = -0.0;
+    double v[kPollPer];
+#pragma unroll
+    for (int k = 0; k < kPollPer; ++k) {
+        const int64_t i = k * 32 + lane;
+        v[k] = i < total ? slot_load(slots + i) : 0.0;
+    }
+    int stage = 0;
+    for (int64_t e0 = 0; e0 < total; e0 += W, stage ^= 1) {
+        double* buf = sbuf + stage * W;
+#pragma unroll
+        for (int k = 0; k < kPollPer; ++k) {
+            const int64_t i = e0 + k * 32 + lane;
+            if (i < total) {
+                while ((unsigned long long)__double_as_longlong(v[k]) == kSlotEmpty) {
+                    __nanosleep(32);
+                    v[k] = slot_load(slots + i);
+                }
+                slot_store(slots + i, empty);
+            }
+            buf[k * 32 + lane] = v[k];
+        }
+        __syncwarp();
+        const int64_t e1 = e0 + W;
+        if (e1 < total) {
+#pragma unroll
+            for (int k = 0; k < kPollPer; ++k) {
+                const int64_t i = e1 + k * 32 + lane;
+                v[k] = i < total ? slot_load(slots + i) : 0.0;
+            }
+        }
+        if (lane < NCH) {
+            const int nw = (int)(total - e0 < W ? total - e0 : W);
+            const int j0 = (int)(((int64_t)lane - e0 % NCH + NCH) % NCH);
+            const int cnt = nw > j0 ? (nw - j0 + NCH - 1) / NCH : 0;
+            tot = chain_fold<NCH>(tot, buf, j0, cnt);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        const double t = __shfl_sync(0xffffffffu, tot, c);
+        if (lane == 0) result[c] = t;
+    }
+}
+
+// Incremental form of stream_fold for a folder warp that also has other
+// work (the SpMV reducer): folds the contiguous ready prefix of the slots
+// from fs->pos on, in whole rows of NCH, and returns when it meets a slot
+// that has not landed (blocking = false) or when all `total` slots are
+// folded (blocking = true).  State lives in shared memory between calls;
+// buf: 32*PER doubles of staging.  Whole warp.
+struct FoldState {
+    long long pos;  // next slot to fold (a multiple of NCH)
+    double tot[4];  // running chains
+};
+
+template <int NCH, int PER>
+__device__ __noinline__ void fold_progress(double* slots, long long total, FoldState* fs, double* buf, bool blocking) {
+    constexpr int W = 32 * PER;
+    const int lane = threadIdx.x & 31;
+    const double empty = __longlong_as_double((long long)kSlotEmpty);
+    long long pos = fs->pos;
+    double tot = lane < NCH ? fs->tot[lane] : 0.0;
+    while (pos < total) {
+        double v[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const long long i = pos + k * 32 + lane;
+            v[k] = i < total ? slot_load(slots + i) : 0.0;
+        }
+        int first_missing = W;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const long long i = pos + k * 32 + lane;
+            const unsigned miss = __ballot_sync(0xffffffffu, i < total && (unsigned long long)__double_as_longlong(v[k]) == kSlotEmpty);
+            if (miss && first_missing == W) first_missing = k * 32 + __ffs(miss) - 1;
+        }
+        long long navail = total - pos < first_missing ? total - pos : first_missing;
+        navail -= navail % NCH;
+        if (navail == 0) {
+            if (!blocking) break;
+            __nanosleep(64);
+            continue;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int j = k * 32 + lane;
+            if (j < navail) {
+                slot_store(slots + pos + j, empty);
+                buf[j] = v[k];
+            }
+        }
+        __syncwarp();
+        if (lane < NCH) tot = chain_fold<NCH>(tot, buf, lane, (int)(navail / NCH));
+        __syncwarp();
+        pos += navail;
+    }
+    if (lane < NCH) fs->tot[lane] = tot;
+    if (lane == 0) fs->pos = pos;
+    __syncwarp();
 }
 
 }  // namespace zk

@@ -99,6 +99,9 @@ struct zk_context {
     char* plan(int32_t L, int32_t kind);
     zk::PlanPtrs plans_for(int64_t n, int64_t block, int32_t kind);
     void* scratch_partials(size_t bytes);
+    // streaming-fold slots (zk_blas1.cu): kept filled with the empty marker
+    double* slots = nullptr;
+    int64_t slots_n = 0;
 };
 
 namespace zk {

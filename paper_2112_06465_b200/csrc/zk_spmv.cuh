@@ -559,6 +559,7 @@ struct RedCfg {
     double* partials;      // nblocks x (2 NC + NR) doubles
     unsigned int* counter; // block arrivals (reset by body.finish)
     int defer;             // row-sharded solve: leave the fold to the cross-rank finish kernel
+    double* slots;         // non-null: streaming fold (zk_blockred.cuh) instead of arrivals + last-CTA fold
 };
 
 constexpr int kPlanCache = 2560;  // bytes of shared memory per cached plan (full-block plans: ~2.0 / 1.3 KB)
@@ -572,7 +573,9 @@ struct RedSmem {
     static constexpr size_t kNodesC = (size_t)kNodeSlots * NC * 16;
     static constexpr size_t kNodesR = (size_t)kNodeSlots * NR * 8;
     static constexpr size_t kPlans = (size_t)kPlanCache * ((NC > 0) + (NR > 0));
-    static constexpr size_t kBytes = (NC + NR) ? kBars + kStashC + kStashR + kNodesC + kNodesR + kPlans : 0;
+    static constexpr int kFoldPer = 8;  // fold_progress staging: 32 x 8 doubles (in the stash, free by then)
+    static constexpr size_t kFold = 64;
+    static constexpr size_t kBytes = (NC + NR) ? kBars + kStashC + kStashR + kNodesC + kNodesR + kPlans + kFold : 0;
     unsigned char* base;
     __device__ uint64_t* sfull() const { return reinterpret_cast<uint64_t*>(base); }
     __device__ uint64_t* sfree() const { return reinterpret_cast<uint64_t*>(base) + kStashSlices; }
@@ -582,6 +585,8 @@ struct RedSmem {
     __device__ double* ndr() const { return reinterpret_cast<double*>(base + kBars + kStashC + kStashR + kNodesC); }
     __device__ char* planc() const { return reinterpret_cast<char*>(base + kBars + kStashC + kStashR + kNodesC + kNodesR); }
     __device__ char* planr() const { return planc() + (NC > 0 ? kPlanCache : 0); }
+    __device__ FoldState* fstate() const { return reinterpret_cast<FoldState*>(planc() + kPlans); }
+    __device__ double* fbuf() const { return reinterpret_cast<double*>(base + kBars); }
 };
 
 // Copies a plan blob into shared memory (whole warp); returns the pointer to
@@ -712,6 +717,7 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
     const int lane = threadIdx.x & 31;
     const char* pc_full = NC ? cache_plan(R.pc.full, sm.planc()) : nullptr;
     const char* pr_full = NR ? cache_plan(R.pr.full, sm.planr()) : nullptr;
+    const bool stream = R.slots != nullptr;
     uint32_t m = 0;  // CTA slice sequence number of the block's first slice
     for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
         const int64_t base = blk * kBlock;
@@ -772,6 +778,20 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
         double pwr[NR > 0 ? NR : 1];
         if constexpr (NC > 0) red_tree<double2, NC>(pcp, sm.ndc(), pwc);
         if constexpr (NR > 0) red_tree<double, NR>(prp, sm.ndr(), pwr);
+        if (stream) {
+            if (lane == 0) {
+                double* S = R.slots + blk * NP;
+#pragma unroll
+                for (int a = 0; a < NC; ++a) {
+                    const double2 t = hc->L > 0 ? cadd(v0c[a], pwc[a]) : v0c[a];
+                    slot_store(S + 2 * a, t.x);
+                    slot_store(S + 2 * a + 1, t.y);
+                }
+#pragma unroll
+                for (int a = 0; a < NR; ++a) slot_store(S + 2 * NC + a, hr->L > 0 ? __dadd_rn(v0r[a], pwr[a]) : v0r[a]);
+            }
+            continue;
+        }
         unsigned int last = 0;
         if (lane == 0) {
             double* P = R.partials + blk * NP;
@@ -794,10 +814,21 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
             __threadfence();
             double tot[NP];
             // the stash is free now (every slice of this CTA was reduced): fold scratch
-            warp_fold<double>(R.partials, NP, A.nblocks, reinterpret_cast<double*>(sm.stc()),
-                              (int)((RedSmem<NC, NR>::kStashC + RedSmem<NC, NR>::kStashR) / (8 * NP)), tot);
+            static_assert(RedSmem<NC, NR>::kStashC + RedSmem<NC, NR>::kStashR >= 2 * kFoldStage * 8, "fold scratch");
+            warp_fold<double>(R.partials, NP, A.nblocks, reinterpret_cast<double*>(sm.stc()), tot);
             if (lane == 0) body.finish(tot);
         }
+    }
+    // streaming fold: the last CTA -- one block fewer than the first CTAs
+    // when the blocks do not divide evenly -- folds the partials in block
+    // order as they land once its own blocks are done (its stash is free:
+    // staging), so the fold overlaps the other CTAs' last blocks
+    if (stream && blockIdx.x == gridDim.x - 1) {
+        if (lane == 0) sm.fstate()->pos = 0;
+        if (lane < NP) sm.fstate()->tot[lane] = -0.0;
+        __syncwarp();
+        fold_progress<NP, RedSmem<NC, NR>::kFoldPer>(R.slots, (long long)A.nblocks * NP, sm.fstate(), sm.fbuf(), true);
+        if (lane == 0) body.finish(sm.fstate()->tot);
     }
 }
 

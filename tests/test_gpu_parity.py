@@ -59,6 +59,25 @@ def test_zdot_znorm2_vs_oracle_large(n):
     assert Z.znorm2(X, Z.ReductionPlan(65536)) == O.znorm2(x, 65536)
 
 
+def test_reductions_signalling_nan_inputs():
+    """The streaming fold marks empty partial slots with a signalling NaN
+    (zk_blas1.cu kSlotEmpty); inputs holding that exact pattern must still
+    give quiet-NaN results, never a hang (arithmetic quiets sNaN)."""
+    snan = np.frombuffer(np.uint64(0x7FF47FF47FF47FF4).tobytes(), dtype=np.float64)[0]
+    for n, bs in ((64 * 5 + 1, 64), (4096 * 3 + 1, 4096), (1, 64)):
+        x = np.ones(n, dtype=np.complex128)
+        x.real[::bs] = snan
+        x.imag[-1] = snan
+        X = Z.ZVector(x)
+        plan = Z.ReductionPlan(bs)
+        assert np.isnan(complex(Z.zdot(X, X, True, plan)).real)
+        assert np.isnan(Z.znorm2(X, plan))
+        y = np.ones(n, dtype=np.complex128)  # and the slots are clean again afterwards
+        Y = Z.ZVector(y)
+        assert complex(Z.zdot(Y, Y, True, plan)) == O.zdot(y, y, True, bs)
+        assert Z.znorm2(Y, plan) == O.znorm2(y, bs)
+
+
 # ---- SpMV ------------------------------------------------------------------------
 
 def test_spmv_golden(spmv_golden):
