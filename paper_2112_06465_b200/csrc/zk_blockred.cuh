@@ -248,7 +248,7 @@ __device__ __forceinline__ bool warp_finish(const char* plan, const V (&v0)[NACC
 // window is folded, and each chain lane reads 16 values into registers
 // ahead of its 16 dependent adds (an LDS per add left the smem latency on
 // the chain: ~19 cycles per partial, measured).
-constexpr int kFoldStage = 512;
+constexpr int kFoldStage = 256;
 
 __device__ __forceinline__ void fold_stream(const double* partials, int nchains, int64_t nb, double* scratch,
                                             double& tot) {

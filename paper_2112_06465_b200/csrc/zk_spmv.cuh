@@ -58,10 +58,17 @@ constexpr int kMaxStages = 32;
 constexpr int kBarBytes = 2 * kMaxStages * 8 + 2 * kMaxStages * 4;  // full, empty mbarriers + stage tags, widths
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kFullCols = 33;  // widest row handled by the whole-row prefetch path
-// Reduction stash: a ring of kStashSlices slice slots (32 rows each) of
+// Reduction stash: a ring of RedSmem::kSlots slice slots (32 rows each) of
 // per-row reduction terms between the consumer warps and the reducer warp.
-constexpr int kStashSlices = 32;
-constexpr int kStashMask = kStashSlices * kSlice - 1;
+// Slots per kernel (powers of two): 16 when the body has complex terms (a
+// smaller stash leaves the TMA ring another stage; the reducer keeps up),
+// 32 for real-only bodies (measured per phase, C4).
+#ifndef ZK_STASH_C
+#define ZK_STASH_C 16
+#endif
+#ifndef ZK_STASH_R
+#define ZK_STASH_R 32
+#endif
 constexpr int kNodeSlots = 136;  // >= plan nodes (<= 129) per accumulator
 
 
@@ -546,7 +553,7 @@ __device__ __noinline__ RowVals<NX> generic_slice(const SellView A, const double
 // ---- fused reductions: consumer warps -> stash ring -> reducer warp --------
 // Per row the body returns NC complex and NR real reduction terms; the
 // consumer warp that owns a slice writes them into stash slot
-// (CTA slice sequence number) % kStashSlices and arrives on that slot's
+// (CTA slice sequence number) % kSlots and arrives on that slot's
 // `sfull` barrier.  The reducer warp takes the slices of each 4096-row block
 // in order, sums every pairwise leaf of the block's plans as soon as all its
 // rows are in (leaf_upto table), releases slots no pending leaf still needs
@@ -567,9 +574,12 @@ constexpr int kLeafBatchRows = 256;  // the reducer sums leaves in batches of ab
 
 template <int NC, int NR>
 struct RedSmem {
-    static constexpr size_t kBars = 2 * kStashSlices * 8;
-    static constexpr size_t kStashC = (size_t)kStashSlices * kSlice * NC * 16;
-    static constexpr size_t kStashR = (size_t)kStashSlices * kSlice * NR * 8;
+    static constexpr int kSlots = NC > 0 ? ZK_STASH_C : ZK_STASH_R;
+    static_assert((kSlots & (kSlots - 1)) == 0, "stash slots: power of two");
+    static constexpr uint32_t kMask = (uint32_t)(kSlots * kSlice - 1);
+    static constexpr size_t kBars = 2 * kSlots * 8;
+    static constexpr size_t kStashC = (size_t)kSlots * kSlice * NC * 16;
+    static constexpr size_t kStashR = (size_t)kSlots * kSlice * NR * 8;
     static constexpr size_t kNodesC = (size_t)kNodeSlots * NC * 16;
     static constexpr size_t kNodesR = (size_t)kNodeSlots * NR * 8;
     static constexpr size_t kPlans = (size_t)kPlanCache * ((NC > 0) + (NR > 0));
@@ -578,7 +588,7 @@ struct RedSmem {
     static constexpr size_t kBytes = (NC + NR) ? kBars + kStashC + kStashR + kNodesC + kNodesR + kPlans + kFold : 0;
     unsigned char* base;
     __device__ uint64_t* sfull() const { return reinterpret_cast<uint64_t*>(base); }
-    __device__ uint64_t* sfree() const { return reinterpret_cast<uint64_t*>(base) + kStashSlices; }
+    __device__ uint64_t* sfree() const { return reinterpret_cast<uint64_t*>(base) + kSlots; }
     __device__ double2* stc() const { return reinterpret_cast<double2*>(base + kBars); }
     __device__ double* str() const { return reinterpret_cast<double*>(base + kBars + kStashC); }
     __device__ double2* ndc() const { return reinterpret_cast<double2*>(base + kBars + kStashC + kStashR); }
@@ -603,11 +613,11 @@ __device__ __forceinline__ const char* cache_plan(const char* g, char* s) {
 }
 
 // Leaves [lo, hi) of `plan` over the stash (segment element e = block row
-// 1 + e at stash row (rowbase + e) & kStashMask).  One (leaf, lane) item per
+// 1 + e at stash row (rowbase + e) & mask).  One (leaf, lane) item per
 // warp lane; the item's <= 16 elements are loaded before the in-order adds.
 template <typename V, int NACC>
 __device__ __forceinline__ void red_leaves(const char* plan, const V* stash, uint32_t rowbase, V* nodes, int lo,
-                                           int hi) {
+                                           int hi, uint32_t mask) {
     constexpr int LANES = VT<V>::lanes;
     constexpr int GMAX = (LANES == 4 ? 64 : 128) / LANES;  // 16
     const PlanHeader* h = reinterpret_cast<const PlanHeader*>(plan);
@@ -618,7 +628,7 @@ __device__ __forceinline__ void red_leaves(const char* plan, const V* stash, uin
 #pragma unroll
             for (int a = 0; a < NACC; ++a) sacc[a] = VT<V>::negzero();
             for (int k = 0; k < h->L; ++k) {
-                const uint32_t r = (rowbase + (uint32_t)k) & kStashMask;
+                const uint32_t r = (rowbase + (uint32_t)k) & mask;
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) sacc[a] = VT<V>::add(sacc[a], stash[r * NACC + a]);
             }
@@ -641,7 +651,7 @@ __device__ __forceinline__ void red_leaves(const char* plan, const V* stash, uin
 #pragma unroll
         for (int g = 0; g < GMAX; ++g) {
             if (g < G) {
-                const uint32_t r = (r0 + (uint32_t)(LANES * g)) & kStashMask;
+                const uint32_t r = (r0 + (uint32_t)(LANES * g)) & mask;
 #pragma unroll
                 for (int a = 0; a < NACC; ++a) vals[g][a] = stash[r * NACC + a];
             }
@@ -667,7 +677,7 @@ __device__ __forceinline__ void red_leaves(const char* plan, const V* stash, uin
         }
         // leftovers (q < rem), added in order by the leaf's lane 0
         V left[NACC];
-        const uint32_t rl = (r0 + (uint32_t)(LANES * G)) & kStashMask;
+        const uint32_t rl = (r0 + (uint32_t)(LANES * G)) & mask;
 #pragma unroll
         for (int a = 0; a < NACC; ++a) left[a] = (valid && q < rem) ? stash[rl * NACC + a] : VT<V>::zero();
         const int grp = lane & ~(LANES - 1);
@@ -736,10 +746,10 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
         double v0r[NR > 0 ? NR : 1];
         for (int j = 0; j < nsl; ++j) {
             const uint32_t sq = m + (uint32_t)j;
-            mbar_wait(&sm.sfull()[sq % kStashSlices], (sq / kStashSlices) & 1);
+            mbar_wait(&sm.sfull()[sq % RedSmem<NC, NR>::kSlots], (sq / RedSmem<NC, NR>::kSlots) & 1);
             const bool lastj = j + 1 == nsl;
             if (j == 0) {
-                const int k0 = (int)((m * kSlice) & kStashMask);
+                const int k0 = (int)((m * kSlice) & RedSmem<NC, NR>::kMask);
 #pragma unroll
                 for (int a = 0; a < NC; ++a) v0c[a] = sm.stc()[k0 * NC + a];
 #pragma unroll
@@ -750,7 +760,7 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
             if constexpr (NC > 0) {
                 const int hi = lastj ? nlc : min((int)hc->leaf_upto[j + 1], nlc);
                 if (hi - lc >= kBatchC || (lastj && hi > lc)) {
-                    red_leaves<double2, NC>(pcp, sm.stc(), rowbase, sm.ndc(), lc, hi);
+                    red_leaves<double2, NC>(pcp, sm.stc(), rowbase, sm.ndc(), lc, hi, RedSmem<NC, NR>::kMask);
                     lc = hi;
                     worked = true;
                 }
@@ -759,7 +769,7 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
             if constexpr (NR > 0) {
                 const int hi = lastj ? nlr : min((int)hr->leaf_upto[j + 1], nlr);
                 if (hi - lr >= kBatchR || (lastj && hi > lr)) {
-                    red_leaves<double, NR>(prp, sm.str(), rowbase, sm.ndr(), lr, hi);
+                    red_leaves<double, NR>(prp, sm.str(), rowbase, sm.ndr(), lr, hi, RedSmem<NC, NR>::kMask);
                     lr = hi;
                     worked = true;
                 }
@@ -769,7 +779,7 @@ __device__ __noinline__ void reducer_warp(const SellView A, Body body, const Red
             if (upto > rel) {
                 if (worked) __syncwarp();  // every lane is done reading the released rows
                 if (lane == 0)
-                    for (int k = rel; k < upto; ++k) mbar_arrive(&sm.sfree()[(m + (uint32_t)k) % kStashSlices]);
+                    for (int k = rel; k < upto; ++k) mbar_arrive(&sm.sfree()[(m + (uint32_t)k) % RedSmem<NC, NR>::kSlots]);
                 rel = upto;
             }
         }
@@ -871,7 +881,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             tag[i] = 0xffffffffu;
         }
         if (kRed) {
-            for (int i = 0; i < kStashSlices; ++i) {
+            for (int i = 0; i < RedSmem<NC, NR>::kSlots; ++i) {
                 mbar_init(&sm.sfull()[i], 1);
                 mbar_init(&sm.sfree()[i], 1);
             }
@@ -1002,8 +1012,8 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             double tr[NR > 0 ? NR : 1];
             if (mine) body.row(row, val.v, svals, tc, tr);
             if (kRed) {
-                if (sq >= (uint32_t)kStashSlices) mbar_wait(&sm.sfree()[sq % kStashSlices], ((sq / kStashSlices) - 1) & 1);
-                const int k = (int)((sq * kSlice + lane) & kStashMask);
+                if (sq >= (uint32_t)RedSmem<NC, NR>::kSlots) mbar_wait(&sm.sfree()[sq % RedSmem<NC, NR>::kSlots], ((sq / RedSmem<NC, NR>::kSlots) - 1) & 1);
+                const int k = (int)((sq * kSlice + lane) & RedSmem<NC, NR>::kMask);
                 if (mine) {
 #pragma unroll
                     for (int a = 0; a < NC; ++a) sm.stc()[k * NC + a] = tc[a];
@@ -1011,7 +1021,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
                     for (int a = 0; a < NR; ++a) sm.str()[k * NR + a] = tr[a];
                 }
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.sfull()[sq % kStashSlices]);
+                if (lane == 0) mbar_arrive(&sm.sfull()[sq % RedSmem<NC, NR>::kSlots]);
             }
         }
         sbase += (uint32_t)nsl;
