@@ -197,7 +197,7 @@ int plan_nnodes(zk_context* c, int32_t L, int32_t kind);
 
 // Slots for the streaming fold, all holding the empty marker between calls
 // (the folder re-marks each slot it consumes).
-static double* fold_slots(zk_context* c, int64_t count) {
+double* fold_slots(zk_context* c, int64_t count) {
     if (count > c->slots_n) {
         if (c->slots) c->alloc.free(c->slots);
         c->slots = static_cast<double*>(c->alloc.alloc(sizeof(double) * count));

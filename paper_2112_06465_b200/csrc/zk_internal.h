@@ -106,4 +106,7 @@ struct zk_context {
 
 namespace zk {
 int num_sms();
+// count doubles of streaming-fold slots (zk_blockred.cuh), all at the empty
+// marker between passes; grown on demand (zk_blas1.cu)
+double* fold_slots(zk_context* c, int64_t count);
 }

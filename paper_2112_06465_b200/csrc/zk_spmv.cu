@@ -311,7 +311,8 @@ void spmv_dot_device(zk_context* c, const zk_csr* A, const double2* x, double2* 
     const PlanPtrs p = c->plans_for(A->n_rows, kBlock, kComplex);
     ZK_CUDA(cudaFuncSetAttribute(k_spmv_dot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k_spmv_dot<<<pipe_grid(A), kRedPipeThreads, smem, c->stream>>>(
-        v, x, SpmvDotBody{y, result, c->counter, conj, c->fma != 0}, RedCfg{p, p, partials, c->counter, 0});
+        v, x, SpmvDotBody{y, result, c->counter, conj, c->fma != 0},
+        RedCfg{p, p, partials, c->counter, 0, fold_slots(c, 2 * (nb ? nb : 1))});
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }
