@@ -89,6 +89,8 @@ struct zk_context {
     unsigned int* counter = nullptr;
     double* d_result = nullptr;    // 4 doubles
     double* h_result = nullptr;    // pinned, 4 doubles
+    char* bounce = nullptr;        // pinned 2 x 8 MB: chunked reads into pageable memory
+    cudaEvent_t bounce_ev[2] = {};
     int64_t launches = 0;          // kernels launched by this context
     cudaEvent_t events[32] = {};   // zk_event_record slots
     bool profile = false;          // zk_profile_enable
