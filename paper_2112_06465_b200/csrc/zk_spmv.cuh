@@ -60,15 +60,14 @@ constexpr int kSmemLimit = 227 * 1024;
 constexpr int kFullCols = 33;  // widest row handled by the whole-row prefetch path
 // Reduction stash: a ring of RedSmem::kSlots slice slots (32 rows each) of
 // per-row reduction terms between the consumer warps and the reducer warp.
-// Slots per kernel (powers of two): 16 when the body has complex terms (a
-// smaller stash leaves the TMA ring another stage; the reducer keeps up),
-// 32 for real-only bodies (measured per phase, C4).
-#ifndef ZK_STASH_C
-#define ZK_STASH_C 16
-#endif
-#ifndef ZK_STASH_R
-#define ZK_STASH_R 32
-#endif
+// Stash slots and reducer leaf batch per body (RedSmem::kSlots, kBatchRows;
+// slots a power of two and above the batch's slices, or the consumers and
+// the reducer deadlock).  Bodies with two complex terms (K4) keep a 16-slot
+// stash and 256-row batches -- the smaller stash gives their TMA ring a
+// stage -- the others take 32 slots and 512-row batches (fewer reducer
+// passes).  Measured on C4, per phase and overall (batch rows / slots):
+// 256/16 1.49, 512/32 1.515, 768/32 1.515, 1024/64 1.47, 128/32 1.30 solves/s;
+// K4 919 us at 256/16 vs 923-941 at 512/32.
 constexpr int kNodeSlots = 136;  // >= plan nodes (<= 129) per accumulator
 
 
@@ -570,12 +569,13 @@ struct RedCfg {
 };
 
 constexpr int kPlanCache = 2560;  // bytes of shared memory per cached plan (full-block plans: ~2.0 / 1.3 KB)
-constexpr int kLeafBatchRows = 256;  // the reducer sums leaves in batches of about this many rows
 
 template <int NC, int NR>
 struct RedSmem {
-    static constexpr int kSlots = NC > 0 ? ZK_STASH_C : ZK_STASH_R;
+    static constexpr int kSlots = NC >= 2 ? 16 : 32;
+    static constexpr int kBatchRows = NC >= 2 ? 256 : 512;  // the reducer sums leaves in batches of ~this many rows
     static_assert((kSlots & (kSlots - 1)) == 0, "stash slots: power of two");
+    static_assert(kSlots * kSlice > kBatchRows, "stash must exceed the reducer's leaf batch");
     static constexpr uint32_t kMask = (uint32_t)(kSlots * kSlice - 1);
     static constexpr size_t kBars = 2 * kSlots * 8;
     static constexpr size_t kStashC = (size_t)kSlots * kSlice * NC * 16;
@@ -723,7 +723,7 @@ __device__ __forceinline__ void red_tree(const char* plan, V* nodes, V (&pw)[NAC
 template <int NC, int NR, class Body>
 __device__ __noinline__ void reducer_warp(const SellView A, Body body, const RedCfg R, RedSmem<NC, NR> sm) {
     constexpr int NP = 2 * NC + NR;
-    constexpr int kBatchC = kLeafBatchRows / 64, kBatchR = kLeafBatchRows / 128;
+    constexpr int kBatchC = RedSmem<NC, NR>::kBatchRows / 64, kBatchR = RedSmem<NC, NR>::kBatchRows / 128;
     const int lane = threadIdx.x & 31;
     const char* pc_full = NC ? cache_plan(R.pc.full, sm.planc()) : nullptr;
     const char* pr_full = NR ? cache_plan(R.pr.full, sm.planr()) : nullptr;
