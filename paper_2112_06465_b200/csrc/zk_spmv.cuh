@@ -67,7 +67,7 @@ constexpr int kFullCols = 33;  // widest row handled by the whole-row prefetch p
 // stage -- the others take 32 slots and 512-row batches (fewer reducer
 // passes).  Measured on C4, per phase and overall (batch rows / slots):
 // 256/16 1.49, 512/32 1.515, 768/32 1.515, 1024/64 1.47, 128/32 1.30 solves/s;
-// K4 919 us at 256/16 vs 923-941 at 512/32.
+// K4 919 us at 256/16 vs 923-941 at 512/32 and 932 at 384/16.
 constexpr int kNodeSlots = 136;  // >= plan nodes (<= 129) per accumulator
 
 
