@@ -55,9 +55,19 @@ DATA = {
 }
 TOL = 1e-8
 MAXIT = 20000
-# Iterations of the C4 solve (bitwise identical between this GPU path and the
-# reference algorithm; the GPU arm re-measures it every run and reports both).
-C4_ITERATIONS_KNOWN = 215  # measured on B200 (bench r01), bitwise the reference algorithm
+# Iteration counts of the BASELINE solves, bitwise identical between this GPU
+# path and the reference algorithm (provenance in the file).  The GPU arm
+# re-measures its count every run and checks it against this record; the
+# reference arm needs it to extrapolate its per-iteration time.
+ITERATIONS_FILE = os.path.join(ROOT, "tests", "golden", "headline_iterations.json")
+
+
+def known_iterations(config: str):
+    try:
+        with open(ITERATIONS_FILE) as fh:
+            return json.load(fh).get(config, {}).get("iterations")
+    except OSError:
+        return None
 
 
 def peaks():
@@ -347,10 +357,9 @@ def run_zk(args, dist: Dist):
         "vs_baseline": None,
         "dtype": "c128 (f64 re/im pairs)",
         "data": DATA[args.config],
-        "config": {
-            "workload": WORKLOADS[args.config],
-            "n": n, "nnz": nnz, "iterations": iters, "converged": bool(rep.converged),
-            "final_rel": rep.final_relative_residual,
+        "config": {"workload": WORKLOADS[args.config], "n": n, "nnz": nnz, "iterations": iters},
+        "detail": {
+            "converged": bool(rep.converged), "final_rel": rep.final_relative_residual,
             "parallelism": "1 GPU",
             "l2": "inputs larger than L2 (4.6 GB matrix, 126 MB L2): no flush",
             "host_setup_s": round(setup_s, 1),
@@ -368,8 +377,26 @@ def run_zk(args, dist: Dist):
         "gpu_launches": int(launches),
         "sub_metrics": sub,
     }
+    known = known_iterations(args.config)
+    out["parity"] = {"iterations_committed": known,
+                     "iterations_match_committed": None if known is None else known == iters}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(ia, ja, aa, b, M.data, iters, args.config)
+        cb, detail = cpu_baseline(ia, ja, aa, b, M.data, iters, args.config)
+        out["cpu_baseline"] = cb
+        # parity of the measured path with the reference algorithm: the CPU
+        # sample's first iteration (residual history prefix and x) against a
+        # 1-iteration solve of the same system on the GPU, bitwise
+        x1, rep1 = Z.solve_bicgstab(A, bv, M, Z.SolverConfig(tolerance=TOL, max_iterations=1))
+        same_fp = cb["host"].get("complex_multiply") == "fma"
+        hist_ok = np.array(rep1.residual_history).tobytes() == np.array(detail["hist"]).tobytes()
+        x_ok = x1.data.tobytes() == detail["x"].tobytes()
+        out["parity"].update({"hist_prefix_bitwise": hist_ok, "x_after_1_iteration_bitwise": x_ok,
+                              "hist_prefix": detail["hist"], "checked_against": "oracle/port.py (numpy) on this host",
+                              "host_fingerprint_matches": same_fp})
+        if same_fp and not (hist_ok and x_ok):
+            raise SystemExit(f"parity failure: GPU {rep1.residual_history} vs reference algorithm {detail['hist']}")
+    if out["parity"]["iterations_match_committed"] is False:
+        raise SystemExit(f"iteration count {iters} differs from the committed bitwise record {known}")
     if dist.rank == 0:
         print(json.dumps(out), flush=True)
 
@@ -445,10 +472,9 @@ def run_sharded(args, dist: Dist):
         "vs_baseline": None,
         "dtype": "c128 (f64 re/im pairs)",
         "data": DATA[args.config],
-        "config": {
-            "workload": WORKLOADS[args.config],
-            "n": n, "nnz": nnz, "iterations": rep.iterations, "converged": bool(rep.converged),
-            "final_rel": rep.final_relative_residual,
+        "config": {"workload": WORKLOADS[args.config], "n": n, "nnz": nnz, "iterations": rep.iterations},
+        "detail": {
+            "converged": bool(rep.converged), "final_rel": rep.final_relative_residual,
             "parallelism": f"row-sharded x{dist.world} ({transport}): 4096-aligned nnz-balanced rows, halo "
                            f"exchange before each SpMV, all-gathered block partials folded in global order",
             "shard_rows": [int(v) for v in np.diff(bounds)], "halo_rows_rank0": shard.n_halo,
@@ -481,7 +507,7 @@ def cpu_sample(ia, ja, aa, b, minv, iters):
     wall = time.perf_counter() - t0
     t_iter = it_times[0]
     per_solve = t_setup + iters * t_iter
-    return 1.0 / per_solve, {"setup_s": t_setup, "iteration_s": t_iter, "wall_s": wall, "hist1": hist[-1]}
+    return 1.0 / per_solve, {"setup_s": t_setup, "iteration_s": t_iter, "wall_s": wall, "hist": list(hist), "x": x}
 
 
 def cpu_baseline(ia, ja, aa, b, minv, iters, config=CONFIG):
@@ -492,19 +518,17 @@ def cpu_baseline(ia, ja, aa, b, minv, iters, config=CONFIG):
             "sample": (f"reference BiCGStab algorithm (oracle/port.py, numpy, single-threaded like zlinalg) on {config}: "
                        f"setup {d['setup_s']:.2f}s + 1 iteration {d['iteration_s']:.2f}s, extrapolated to "
                        f"{iters} iterations"),
-            "host": facts}
+            "host": facts}, d
 
 
 def run_reference(args, dist: Dist):
     if dist.rank != 0:
         return
-    iters = args.iterations
+    iters = args.iterations if args.iterations is not None else known_iterations(args.config)
     if iters is None:
-        iters = C4_ITERATIONS_KNOWN
-    if iters is None:
-        print(json.dumps({"impl": "reference", "unavailable": "C4 iteration count unknown; pass --iterations"}))
+        print(json.dumps({"impl": "reference", "unavailable": f"{args.config} iteration count unknown; pass --iterations"}))
         return
-    n, ia, ja, aa, b = build_problem()
+    n, ia, ja, aa, b = build_problem(args.config)
     diag = np.zeros(n, dtype=np.complex128)
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(ia))
     hit = rows == ja
@@ -518,15 +542,16 @@ def run_reference(args, dist: Dist):
         vals.append(v)
         details.append(d)
     value = statistics.median(vals)
-    sample = (f"reference BiCGStab algorithm (oracle/port.py, numpy) on C4, per step: setup + 1 iteration "
+    sample = (f"reference BiCGStab algorithm (oracle/port.py, numpy) on {args.config}, per step: setup + 1 iteration "
               f"(median iteration {statistics.median(d['iteration_s'] for d in details):.2f}s), extrapolated to "
               f"{iters} iterations")
     out = {"metric": "bicgstab_solves_per_sec", "value": value, "unit": "solves/s", "n_gpus": dist.world,
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": statistics.median(d["wall_s"] for d in details) * 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64 re/im pairs)", "data": "synthetic",
-           "config": {"workload": "C4: 27-point Helmholtz 200^3, k^2=100, eps=0.05, Jacobi BiCGStab tol 1e-8",
-                      "iterations": iters},
+           "config": {"workload": WORKLOADS[args.config], "n": n, "nnz": int(ia[-1]), "iterations": iters},
+           "detail": {"iterations_source": "tests/golden/headline_iterations.json (bitwise GPU == oracle)",
+                      "parallelism": "1 host core (numpy ufuncs are single-threaded; the hot path calls no BLAS)"},
            "impl": "reference",
            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": 1, "kind": "port", "sample": sample},
            "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -539,7 +564,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["zk", "reference"], default="zk")
-    ap.add_argument("--iterations", type=int, default=None, help="reference arm: C4 iteration count")
+    ap.add_argument("--iterations", type=int, default=None, help="reference arm: override the committed iteration count")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default=CONFIG, help="BASELINE system (default C4)")
     args = ap.parse_args()

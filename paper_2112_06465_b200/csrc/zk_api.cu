@@ -35,6 +35,7 @@ size_t Allocator::round(size_t b) {
 }
 
 void* Allocator::alloc(size_t bytes) {
+    std::lock_guard<std::recursive_mutex> lk(mu_);
     const size_t r = round(bytes);
     auto it = cache_.find(r);
     void* p = nullptr;
@@ -60,6 +61,7 @@ void* Allocator::alloc(size_t bytes) {
 
 void Allocator::free(void* p) {
     if (!p) return;
+    std::lock_guard<std::recursive_mutex> lk(mu_);
     auto it = live_.find(p);
     if (it == live_.end()) throw ZkError{ZK_ERR_PARAMETER, "zk_free: pointer not owned by this context"};
     cache_[it->second].push_back(p);
@@ -68,6 +70,7 @@ void Allocator::free(void* p) {
 }
 
 void Allocator::release_cached() {
+    std::lock_guard<std::recursive_mutex> lk(mu_);
     for (auto& kv : cache_)
         for (void* p : kv.second) cudaFree(p);
     cache_.clear();

@@ -72,6 +72,10 @@ struct SolverPlan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     bool graph_ok = false;
+    // arithmetic the graph's kernel parameters were captured with: the FMA
+    // fingerprint and numpy's elision swap (SellView::swap, which depends on
+    // zk_context::elide_bytes); a change of either rebuilds the graph
+    bool graph_fma = true, graph_swap = false;
 };
 
 namespace {
@@ -742,8 +746,9 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     const int64_t n = A->n_rows;
     SolverPlan* P = get_plan(c, A, minv != nullptr, maxit);
     SolverBufs& B = P->bufs;
-    if (B.fma != (c->fma != 0)) {  // fingerprint changed since the graph was built
-        B.fma = c->fma != 0;
+    const bool swap = A->nnz_elide * 16 >= c->elide_bytes;
+    B.fma = c->fma != 0;
+    if (P->graph_ok && (P->graph_fma != B.fma || P->graph_swap != swap)) {  // arithmetic changed since capture
         if (P->exec) cudaGraphExecDestroy(P->exec);
         if (P->graph) cudaGraphDestroy(P->graph);
         P->exec = nullptr;
@@ -767,7 +772,11 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     Launch L = make_launch(c, A, P);
     SolverState out;
     if (use_graph() && !c->profile) {
-        if (!P->graph_ok) build_graph(L);
+        if (!P->graph_ok) {
+            build_graph(L);
+            P->graph_fma = B.fma;
+            P->graph_swap = swap;
+        }
         ZK_CUDA(cudaGraphLaunch(P->exec, s));
         ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
         ZK_CUDA(cudaStreamSynchronize(s));
@@ -889,6 +898,10 @@ void* dist_vector(DistSolver* D, int which, int64_t* len) {
 void dist_reset(DistSolver* D, double tol, int64_t maxit, bool has_x0) {
     SolverBufs& B = D->P->bufs;
     if (maxit + 1 > D->P->hist_cap) throw ZkError{ZK_ERR_PARAMETER, "max_iterations above the shard's capacity"};
+    // the launch parameters carry the arithmetic fingerprint (SellView::fma,
+    // ::swap, SolverBufs::fma): rebuild them in case zk_set_arith changed it
+    B.fma = D->c->fma != 0;
+    D->L = make_launch(D->c, D->A, D->P);
     cudaStream_t s = D->c->stream;
     const size_t vb = sizeof(double2) * (size_t)D->n_ext;
     if (!has_x0) ZK_CUDA(cudaMemsetAsync(B.x, 0, vb, s));

@@ -35,6 +35,8 @@ struct ZkError {
 
 // Size-class caching allocator over cudaMalloc (cudaFree synchronises the
 // device, and the reference test-suite creates thousands of small vectors).
+// Thread-safe: ctypes releases the GIL during calls, so a DeviceBuffer's
+// finaliser may free on one thread while another call allocates.
 class Allocator {
 public:
     void* alloc(size_t bytes);
@@ -48,6 +50,7 @@ private:
     std::map<size_t, std::vector<void*>> cache_;
     std::map<void*, size_t> live_;
     size_t in_use_ = 0;
+    std::recursive_mutex mu_;
 };
 
 struct SolverPlan;  // zk_bicgstab.cu

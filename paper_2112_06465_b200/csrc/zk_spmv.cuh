@@ -575,7 +575,11 @@ struct RedSmem {
     static constexpr int kSlots = NC >= 2 ? 16 : 32;
     static constexpr int kBatchRows = NC >= 2 ? 256 : 512;  // the reducer sums leaves in batches of ~this many rows
     static_assert((kSlots & (kSlots - 1)) == 0, "stash slots: power of two");
-    static_assert(kSlots * kSlice > kBatchRows, "stash must exceed the reducer's leaf batch");
+    // Deadlock freedom: the reducer may hold a whole leaf batch, plus one
+    // partially covered leaf (<= 64 complex / 128 real rows), plus up to a
+    // slice of misalignment, while the consumers need the slice being
+    // waited on -- all of it must fit in the stash at once.
+    static_assert(kSlots * kSlice >= kBatchRows + 128 + 2 * kSlice, "stash too small for the reducer's leaf batch");
     static constexpr uint32_t kMask = (uint32_t)(kSlots * kSlice - 1);
     static constexpr size_t kBars = 2 * kSlots * 8;
     static constexpr size_t kStashC = (size_t)kSlots * kSlice * NC * 16;

@@ -52,35 +52,51 @@ class SolverConfig:
 
 
 class Preconditioner:
-    """Right preconditioner: ``identity`` or ``jacobi`` (stored inverse diagonal
-    ``data``, complex128, host array; a device copy is cached on first use)."""
+    """Right preconditioner: ``identity`` or ``jacobi`` (krylov.py:75-100).
 
-    __slots__ = ("kind", "data", "_dev")
+    ``data`` is the stored inverse diagonal (a complex128 array, as in the
+    reference).  It lives in a :class:`ZVector`, so the device copy follows
+    the same residency rules as any vector: handing ``data`` out marks the
+    device copy stale (the caller may edit it in place), and the next solve
+    re-uploads it."""
 
-    def __init__(self, kind: str, data: np.ndarray | None = None):
+    __slots__ = ("kind", "_minv")
+
+    def __init__(self, kind: str, data=None):
         if kind not in ("identity", "jacobi"):
             raise ParameterError(f"unknown preconditioner kind {kind!r}")
         if kind == "jacobi" and data is None:
             raise ParameterError("jacobi preconditioner needs the inverse diagonal")
         self.kind = kind
-        self.data = data
-        self._dev = None
+        self._minv = None
+        if data is not None:
+            self.data = data
+
+    @property
+    def data(self):
+        return None if self._minv is None else self._minv.data
+
+    @data.setter
+    def data(self, value):
+        self._minv = value if isinstance(value, ZVector) else ZVector(np.asarray(value, dtype=np.complex128))
+
+    @property
+    def size(self) -> int:
+        return len(self._minv) if self._minv is not None else 0
 
     @classmethod
     def identity(cls) -> "Preconditioner":
         return cls("identity")
 
     def _device_minv(self) -> ZVector:
-        if self._dev is None or self._dev[0] is not self.data:
-            self._dev = (self.data, ZVector(np.asarray(self.data, dtype=np.complex128)))
-        return self._dev[1]
+        return self._minv
 
     def apply(self, v: ZVector) -> ZVector:
         """M^-1 v as a new vector (krylov.py:92-100)."""
         if self.kind == "identity":
             return v.copy()
-        if self.data.shape[0] != len(v):
-            raise DimensionError(f"preconditioner built for size {self.data.shape[0]}, vector has {len(v)}")
+        if self.size != len(v):
+            raise DimensionError(f"preconditioner built for size {self.size}, vector has {len(v)}")
         out = ZVector._device_new(len(v))
         if len(v):
             m = self._device_minv()._dptr()
@@ -125,8 +141,8 @@ def solve_bicgstab(A, b, M=None, cfg=None):
     if len(b) != n:
         raise DimensionError(f"matrix is {n}x{n} but right-hand side has {len(b)} elements")
     M = M if M is not None else Preconditioner.identity()
-    if M.kind == "jacobi" and M.data.shape[0] != n:
-        raise DimensionError(f"preconditioner built for size {M.data.shape[0]}, matrix is {n}x{n}")
+    if M.kind == "jacobi" and M.size != n:
+        raise DimensionError(f"preconditioner built for size {M.size}, matrix is {n}x{n}")
     t0 = time.perf_counter()
     guess = cfg.initial_guess
     if guess is not None and len(guess) != n:

@@ -4,13 +4,14 @@ Not on the hot path: these build the CSR inputs (``ia``/``ja`` int64,
 ``aa`` complex128, exactly the reference ``CsrMatrix`` layout,
 ``sparse.py:60-103``) that the solver consumes.  They are vectorised numpy
 replacements for the reference's per-row Python loop
-(``helmholtz.py:206-259``), which needs ~4.5 s per million rows.
+(``helmholtz.py:115-168``, ``assemble``), which needs ~4.5 s per million rows.
 
 * :func:`helmholtz_fd` -- the reference's (2*dim+1)-point central-difference
   stencil with a unit interior source and zero Dirichlet data, i.e. what
-  ``assemble(load_problem_config(...))`` produces (``helmholtz.py:302-339``).
-  With ``damping == 0`` the arrays are bitwise identical to the reference
-  (checked by ``tests/test_problems.py`` against fixtures made from it).
+  ``assemble(load_problem_config(...))`` produces (``helmholtz.py:115-168``,
+  ``:211-249``).  With ``damping == 0`` the arrays are bitwise identical to the
+  reference (checked by ``tests/test_oracle.py`` against ``tests/golden/problems.npz``,
+  made from it by ``tests/golden/make_golden.py``).
   ``damping = eps`` shifts the diagonal by ``-i * eps * k^2`` (complex
   damping ``k^2 (1 + i eps)``; BASELINE configs C1/C5).
 * :func:`helmholtz_27pt` -- 27-point stencil, diagonal ``26/(3h^2) - k^2(1+i eps)``,

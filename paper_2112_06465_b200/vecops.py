@@ -73,16 +73,21 @@ class ZVector:
         return cls(np.array([complex(v) for v in values], dtype=np.complex128))
 
     def copy(self) -> "ZVector":
-        if self._dev_ok and not self._host_ok:
+        """Fresh vector with the same contents; stays on the device when the
+        device copy is current (neither side of the source is invalidated)."""
+        if self._dev_ok and self._n:
             out = ZVector._device_new(self._n)
-            if self._n:
-                _lib.check(_lib.lib().zk_memcpy_d2d(_lib.context(), out._dev.ptr, self._dev.ptr, 16 * self._n))
+            _lib.check(_lib.lib().zk_memcpy_d2d(_lib.context(), out._dev.ptr, self._dev.ptr, 16 * self._n))
             return out
-        return ZVector(self.data.copy())
+        return ZVector(self._host_view().copy())
 
     # -- residency ------------------------------------------------------------
     @property
     def data(self) -> np.ndarray:
+        """The host array (the reference's ``.data``).  Callers may write
+        through it (test_vecops.py:262-266, test_acceptance.py:146-148), so
+        handing it out marks the device copy stale; the library's own
+        read-only accesses go through ``_host_view`` instead."""
         if not self._host_ok:
             if self._host is None:
                 self._host = np.empty(self._n, dtype=np.complex128)
