@@ -31,6 +31,17 @@ BREAKDOWN_NAMES = {
     3: "shadow pivot <r~, A M^-1 p>",
     4: "omega denominator <t, t>",
 }
+# BiCGSTAB(l) / TFQMR breakdown codes (krylov.py:298-489): name for the
+# reference's BreakdownError text; 5 carries the basis-vector index j
+EXT_BREAKDOWN_NAMES = {
+    1: "rho",
+    2: "omega",
+    3: "shadow pivot",
+    5: "minimal-residual basis vector {j}",
+    6: "sigma = <r~, v>",
+    7: "alpha",
+    8: "quasi-residual tau",
+}
 
 
 def build() -> str:
@@ -56,6 +67,13 @@ def lib():
         L.zko_bicgstab.argtypes = [ctypes.c_int64, _I, _I, _D, _D, _D, _D, ctypes.c_double,
                                    ctypes.c_int64, _D, _D, _I, ctypes.POINTER(ctypes.c_int)]
         L.zko_bicgstab.restype = ctypes.c_int
+        _IP = ctypes.POINTER(ctypes.c_int)
+        L.zko_bicgstab_l.argtypes = [ctypes.c_int64, _I, _I, _D, _D, _D, _D, ctypes.c_double, ctypes.c_int64,
+                                     ctypes.c_int, _D, _D, _I, _IP, _IP]
+        L.zko_bicgstab_l.restype = ctypes.c_int
+        L.zko_tfqmr.argtypes = [ctypes.c_int64, _I, _I, _D, _D, _D, _D, ctypes.c_double, ctypes.c_int64, _D, _D,
+                                _I, _IP]
+        L.zko_tfqmr.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -148,3 +166,40 @@ def bicgstab(n, ia, ja, aa, b, minv=None, x0=None, tol=1e-9, maxit=1000):
                             ctypes.byref(iters), ctypes.byref(what))
     k = iters.value
     return x, hist[: k + 1].tolist(), k, st, what.value
+
+
+def bicgstab_l(n, ia, ja, aa, b, minv=None, x0=None, tol=1e-9, maxit=1000, ell=8):
+    """krylov.py:298-410.  Returns (x, history, iterations, status, what, what_j)."""
+    ia, ja, aa, b = _i64(ia), _i64(ja), _c128(aa), _c128(b)
+    minv = _c128(minv) if minv is not None else None
+    x0 = _c128(x0) if x0 is not None else None
+    x = np.empty(int(n), dtype=np.complex128)
+    hist = np.zeros(int(maxit) + 1)
+    iters = ctypes.c_int64(0)
+    what, what_j = ctypes.c_int(0), ctypes.c_int(0)
+    st = lib().zko_bicgstab_l(int(n), ia.ctypes.data_as(_I), ja.ctypes.data_as(_I), _dp(aa), _dp(b), _dp(minv),
+                              _dp(x0), float(tol), int(maxit), int(ell), _dp(x), _dp(hist), ctypes.byref(iters),
+                              ctypes.byref(what), ctypes.byref(what_j))
+    k = iters.value
+    return x, hist[: k + 1].tolist(), k, st, what.value, what_j.value
+
+
+def tfqmr(n, ia, ja, aa, b, minv=None, x0=None, tol=1e-9, maxit=1000):
+    """krylov.py:413-489.  Returns (x, history, iterations, status, what)."""
+    ia, ja, aa, b = _i64(ia), _i64(ja), _c128(aa), _c128(b)
+    minv = _c128(minv) if minv is not None else None
+    x0 = _c128(x0) if x0 is not None else None
+    x = np.empty(int(n), dtype=np.complex128)
+    hist = np.zeros(int(maxit) + 1)
+    iters = ctypes.c_int64(0)
+    what = ctypes.c_int(0)
+    st = lib().zko_tfqmr(int(n), ia.ctypes.data_as(_I), ja.ctypes.data_as(_I), _dp(aa), _dp(b), _dp(minv),
+                         _dp(x0), float(tol), int(maxit), _dp(x), _dp(hist), ctypes.byref(iters), ctypes.byref(what))
+    k = iters.value
+    return x, hist[: k + 1].tolist(), k, st, what.value
+
+
+def breakdown_message(what: int, what_j: int, iterations: int, ext: bool = True) -> str:
+    """The reference's BreakdownError text (krylov.py:200-206)."""
+    name = (EXT_BREAKDOWN_NAMES if ext else BREAKDOWN_NAMES)[what].format(j=what_j)
+    return f"{name} numerically zero (|value| < 1e-300) after {iterations} iterations"

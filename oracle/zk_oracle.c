@@ -403,3 +403,228 @@ done:
     free(r); free(rs); free(p); free(v); free(s); free(t); free(ph); free(sh); free(t1); free(t2);
     return status;
 }
+
+/* ---- BiCGSTAB(l) and TFQMR (krylov.py:298-489) ------------------------------
+ * Breakdown codes shared with the device drivers (include/zk.h ZK_BD_*):
+ * 1 rho, 2 omega, 3 shadow pivot, 5 minimal-residual basis vector j
+ * (*what_j_out = j), 6 sigma = <r~, v>, 7 alpha, 8 quasi-residual tau. */
+enum { ZKO_BD_MR = 5, ZKO_BD_SIGMA = 6, ZKO_BD_ALPHA = 7, ZKO_BD_TAU = 8 };
+
+static int small_r(double v) { return fabs(v) < 1e-300; }
+static zc zc_neg(zc a) { zc r = {-a.re, -a.im}; return r; }
+static zc zc_add(zc a, zc b) { zc r = {a.re + b.re, a.im + b.im}; return r; }
+static zc zc_sub(zc a, zc b) { zc r = {a.re - b.re, a.im - b.im}; return r; }
+static zc zc_real(double v) { zc r = {v, 0.0}; return r; }
+static void axpy_c(int64_t n, zc a, const zc* x, zc* y) { zko_zaxpy(n, a.re, a.im, (const double*)x, (double*)y); }
+static void scal_c(int64_t n, zc a, zc* x) { zko_zscal(n, a.re, a.im, (double*)x); }
+
+/* op(v) = spmv(A, M.apply(v)) (krylov.py:320-321) */
+static void op_apply(zko_run* R, const zc* v, zc* tmp, zc* out) {
+    precond(R, v, tmp);
+    zko_spmv(R->n, R->n, R->ia, R->ja, R->aa, (const double*)tmp, (double*)out);
+}
+
+/* _Run.__init__ + trivial_result (krylov.py:147-181).  Returns 1 when the
+ * solve is trivially finished (status in *status). */
+static int run_setup(zko_run* R, const zc* x0, zc* x, zc* r0, zc* tmp, double tol, double* hist,
+                     double* r0_norm, int* status) {
+    int64_t n = R->n;
+    if (x0) memcpy(x, x0, sizeof(zc) * (size_t)n);
+    else memset(x, 0, sizeof(zc) * (size_t)n);
+    R->b_norm = nrm_def(n, (const zc*)R->b);
+    zko_spmv(n, n, R->ia, R->ja, R->aa, (const double*)x, (double*)tmp);
+    memcpy(r0, R->b, sizeof(zc) * (size_t)n);
+    zko_zaxpy(n, -1.0, 0.0, (const double*)tmp, (double*)r0);
+    *r0_norm = nrm_def(n, r0);
+    hist[0] = R->b_norm > 0.0 ? *r0_norm / R->b_norm : 0.0;
+    if (R->b_norm == 0.0) {
+        memset(x, 0, sizeof(zc) * (size_t)n);
+        hist[0] = 0.0;
+        *status = ZKO_CONVERGED;
+        return 1;
+    }
+    if (hist[0] <= tol) { *status = ZKO_CONVERGED; return 1; }
+    return 0;
+}
+
+/* current_x(acc) = x0 + M^-1 acc (krylov.py:323-326) */
+static void current_x(zko_run* R, const zc* x0, const zc* acc, zc* tmp, zc* x) {
+    if (x0) memcpy(x, x0, sizeof(zc) * (size_t)R->n);
+    else memset(x, 0, sizeof(zc) * (size_t)R->n);
+    precond(R, acc, tmp);
+    axpy_c(R->n, zc_real(1.0), tmp, x);
+}
+
+int zko_bicgstab_l(int64_t n, const int64_t* ia, const int64_t* ja, const double* aa,
+                   const double* b, const double* minv, const double* x0d, double tol,
+                   int64_t maxit, int ell, double* x_out, double* hist, int64_t* iters_out,
+                   int* what_out, int* what_j_out) {
+    zko_run R = {n, n, ia, ja, aa, b, minv, 0.0};
+    const zc* x0 = (const zc*)x0d;
+    size_t bytes = sizeof(zc) * (size_t)(n > 0 ? n : 1);
+    zc* x = (zc*)x_out;
+    zc *tmp = malloc(bytes), *t2 = malloc(bytes), *acc = calloc(1, bytes), *rs = malloc(bytes);
+    if (ell < 1) ell = 1;
+    zc** r = malloc(sizeof(zc*) * (size_t)(ell + 1));
+    zc** u = malloc(sizeof(zc*) * (size_t)(ell + 1));
+    for (int i = 0; i <= ell; ++i) { r[i] = calloc(1, bytes); u[i] = calloc(1, bytes); }
+    int L1 = ell + 1;
+    zc* tau = calloc((size_t)L1 * L1, sizeof(zc));
+    double* sigma = calloc((size_t)L1, sizeof(double));
+    zc *gp = calloc((size_t)L1, sizeof(zc)), *gm = calloc((size_t)L1, sizeof(zc)), *gpp = calloc((size_t)L1, sizeof(zc));
+    int status = ZKO_NOT_CONVERGED;
+    int64_t it = 0;
+    double r0_norm;
+    *what_out = ZKO_BD_NONE;
+    *what_j_out = 0;
+    if (run_setup(&R, x0, x, r[0], tmp, tol, hist, &r0_norm, &status)) goto done;
+    memcpy(rs, r[0], bytes);
+    zc rho = zc_real(1.0), alpha = zc_real(0.0), omega = zc_real(1.0);
+    while (it < maxit) {
+        if (small_py(omega)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_OMEGA; goto done; }
+        rho = cmul_py(zc_neg(omega), rho);
+        for (int j = 0; j < ell; ++j) {
+            zc rho_next;
+            dot_def(n, rs, r[j], &rho_next);
+            if (small_py(rho)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_RHO; goto done; }
+            zc beta = cmul_py(alpha, cdiv_py(rho_next, rho));
+            rho = rho_next;
+            for (int i = 0; i <= j; ++i) {
+                scal_c(n, zc_neg(beta), u[i]);
+                axpy_c(n, zc_real(1.0), r[i], u[i]);
+            }
+            op_apply(&R, u[j], tmp, u[j + 1]);
+            zc pivot;
+            dot_def(n, rs, u[j + 1], &pivot);
+            if (small_py(pivot)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_PIVOT; goto done; }
+            alpha = cdiv_py(rho, pivot);
+            for (int i = 0; i <= j; ++i) axpy_c(n, zc_neg(alpha), u[i + 1], r[i]);
+            op_apply(&R, r[j], tmp, r[j + 1]);
+            axpy_c(n, alpha, u[0], acc);
+            if (nrm_def(n, r[0]) / R.b_norm <= tol) {
+                current_x(&R, x0, acc, tmp, x);
+                double rel = true_rel(&R, x, tmp, t2);
+                if (rel <= tol) { hist[++it] = rel; status = ZKO_CONVERGED; goto done; }
+            }
+        }
+        for (int j = 1; j <= ell; ++j) {
+            for (int i = 1; i < j; ++i) {
+                zc d;
+                dot_def(n, r[i], r[j], &d);
+                zc tij = cdiv_py(d, zc_real(sigma[i]));
+                tau[i * L1 + j] = tij;
+                axpy_c(n, zc_neg(tij), r[i], r[j]);
+            }
+            zc sg;
+            dot_def(n, r[j], r[j], &sg);
+            sigma[j] = sg.re;
+            if (small_r(sigma[j])) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_MR; *what_j_out = j; goto done; }
+            zc g;
+            dot_def(n, r[j], r[0], &g);
+            gp[j] = cdiv_py(g, zc_real(sigma[j]));
+        }
+        for (int j = 0; j <= ell; ++j) gm[j] = zc_real(0.0);
+        gm[ell] = gp[ell];
+        omega = gm[ell];
+        for (int j = ell - 1; j >= 1; --j) {
+            zc s = zc_real(0.0);
+            for (int i = j + 1; i <= ell; ++i) s = zc_add(s, cmul_py(tau[j * L1 + i], gm[i]));
+            gm[j] = zc_sub(gp[j], s);
+        }
+        for (int j = 1; j < ell; ++j) {
+            zc s = zc_real(0.0);
+            for (int i = j + 1; i < ell; ++i) s = zc_add(s, cmul_py(tau[j * L1 + i], gm[i + 1]));
+            gpp[j] = zc_add(gm[j + 1], s);
+        }
+        axpy_c(n, gm[1], r[0], acc);
+        axpy_c(n, zc_neg(gp[ell]), r[ell], r[0]);
+        axpy_c(n, zc_neg(gm[ell]), u[ell], u[0]);
+        for (int j = 1; j < ell; ++j) {
+            axpy_c(n, zc_neg(gm[j]), u[j], u[0]);
+            axpy_c(n, gpp[j], r[j], acc);
+            axpy_c(n, zc_neg(gp[j]), r[j], r[0]);
+        }
+        current_x(&R, x0, acc, tmp, x);
+        double rel = true_rel(&R, x, tmp, t2);
+        hist[++it] = rel;
+        if (rel <= tol) { status = ZKO_CONVERGED; goto done; }
+    }
+done:
+    *iters_out = it;
+    for (int i = 0; i <= ell; ++i) { free(r[i]); free(u[i]); }
+    free(r); free(u); free(tmp); free(t2); free(acc); free(rs); free(tau); free(sigma); free(gp); free(gm); free(gpp);
+    return status;
+}
+
+int zko_tfqmr(int64_t n, const int64_t* ia, const int64_t* ja, const double* aa,
+              const double* b, const double* minv, const double* x0d, double tol,
+              int64_t maxit, double* x_out, double* hist, int64_t* iters_out, int* what_out) {
+    zko_run R = {n, n, ia, ja, aa, b, minv, 0.0};
+    size_t bytes = sizeof(zc) * (size_t)(n > 0 ? n : 1);
+    zc* x = (zc*)x_out;
+    zc *r0 = malloc(bytes), *w = malloc(bytes), *y = malloc(bytes), *rs = malloc(bytes), *d = calloc(1, bytes),
+       *z = malloc(bytes), *uv = malloc(bytes), *uo = malloc(bytes), *v = malloc(bytes), *t1 = malloc(bytes),
+       *t2 = malloc(bytes);
+    int status = ZKO_NOT_CONVERGED;
+    int64_t it = 0;
+    double r0_norm;
+    *what_out = ZKO_BD_NONE;
+    if (run_setup(&R, (const zc*)x0d, x, r0, t1, tol, hist, &r0_norm, &status)) goto done;
+    memcpy(w, r0, bytes);
+    memcpy(y, r0, bytes);
+    memcpy(rs, r0, bytes);
+    precond(&R, y, z);
+    zko_spmv(n, n, ia, ja, aa, (const double*)z, (double*)uv);
+    memcpy(v, uv, bytes);
+    double theta = 0.0, tau = r0_norm;
+    zc eta = zc_real(0.0), rho;
+    dot_def(n, rs, r0, &rho);
+    while (it < maxit) {
+        zc sigma;
+        dot_def(n, rs, v, &sigma);
+        if (small_py(sigma)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_SIGMA; goto done; }
+        zc alpha = cdiv_py(rho, sigma);
+        if (small_py(alpha)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_ALPHA; goto done; }
+        double rel = INFINITY;
+        int converged = 0;
+        for (int half = 0; half < 2; ++half) {
+            if (half == 1) {
+                axpy_c(n, zc_neg(alpha), v, y);
+                precond(&R, y, z);
+                zko_spmv(n, n, ia, ja, aa, (const double*)z, (double*)uv);
+            }
+            axpy_c(n, zc_neg(alpha), uv, w);
+            /* (theta * theta) * eta / alpha: Cplx.__rmul__ = cmul(eta, theta^2), then cdiv */
+            scal_c(n, cdiv_py(cmul_py(eta, zc_real(theta * theta)), alpha), d);
+            axpy_c(n, zc_real(1.0), z, d);
+            if (small_r(tau)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_TAU; goto done; }
+            theta = nrm_def(n, w) / tau;
+            double c = 1.0 / sqrt(1.0 + theta * theta);
+            tau = tau * theta * c;
+            eta = cmul_py(alpha, zc_real(c * c));
+            axpy_c(n, eta, d, x);
+            rel = true_rel(&R, x, t1, t2);
+            if (rel <= tol) { converged = 1; break; }
+        }
+        hist[++it] = rel;
+        if (converged) { status = ZKO_CONVERGED; goto done; }
+        zc rho_next;
+        dot_def(n, rs, w, &rho_next);
+        if (small_py(rho)) { status = ZKO_BREAKDOWN; *what_out = ZKO_BD_RHO; goto done; }
+        zc beta = cdiv_py(rho_next, rho);
+        rho = rho_next;
+        scal_c(n, beta, y);
+        axpy_c(n, zc_real(1.0), w, y);
+        zc* tmp = uo; uo = uv; uv = tmp;  /* u_old = uvec */
+        precond(&R, y, z);
+        zko_spmv(n, n, ia, ja, aa, (const double*)z, (double*)uv);
+        scal_c(n, beta, v);
+        axpy_c(n, zc_real(1.0), uo, v);
+        scal_c(n, beta, v);
+        axpy_c(n, zc_real(1.0), uv, v);
+    }
+done:
+    *iters_out = it;
+    free(r0); free(w); free(y); free(rs); free(d); free(z); free(uv); free(uo); free(v); free(t1); free(t2);
+    return status;
+}

@@ -108,3 +108,28 @@ def test_27pt_generator_structure():
     within = np.diff(ja)[np.diff(rows) == 0]
     assert np.all(within > 0)
     assert np.all(aa[ja == rows] == aa[0])
+
+
+def test_oracle_krylov_ext_bitwise():
+    """BiCGSTAB(l) / TFQMR restatements vs fixtures from the live reference
+    (krylov.py:298-489): history, status, breakdown text and solution."""
+    from conftest import golden_cases, load_golden
+    for case, g in golden_cases(load_golden("krylov_ext")).items():
+        n = g["b"].shape[0]
+        tol, maxit, ell = g["params"]
+        minv = g["minv"] if g["minv"].size else None
+        guess = g["guess"] if g["guess"].size else None
+        if str(g["solver"][0]) == "bicgstabl":
+            x, hist, it, st, what, wj = O.bicgstab_l(n, g["ia"], g["ja"], g["aa"], g["b"], minv, guess, float(tol),
+                                                     int(maxit), int(ell))
+        else:
+            x, hist, it, st, what = O.tfqmr(n, g["ia"], g["ja"], g["aa"], g["b"], minv, guess, float(tol), int(maxit))
+            wj = 0
+        assert np.asarray(hist).tobytes() == g["hist"].tobytes(), case
+        status = str(g["status"][0])
+        if status == "breakdown":
+            assert st == O.STATUS_BREAKDOWN, case
+            assert O.breakdown_message(what, wj, it) == str(g["what"][0]), case
+        else:
+            assert st == (O.STATUS_CONVERGED if status == "converged" else O.STATUS_NOT_CONVERGED), case
+            assert same_bits(x, g["x"]), case
