@@ -163,6 +163,28 @@ zk_status zk_bicgstab(zk_context* ctx, const zk_csr* A, const double* b, const d
                       const double* x0, double tolerance, int64_t max_iterations, double* x_out,
                       double* history_host, zk_solve_report* report);
 
+/* ---- BiCGSTAB(l) and TFQMR (krylov.py:298-489) ------------------------------
+ * Device-resident like zk_bicgstab: one CUDA-graph launch per solve (a
+ * conditional WHILE over one outer cycle of BiCGSTAB(l), resp. two TFQMR
+ * iterations), scalars and control flow on the device, one host wait.
+ * report->breakdown holds a ZK_BD_* code; for ZK_BD_MR *breakdown_index is
+ * the basis vector j of "minimal-residual basis vector {j}". */
+#define ZK_BD_RHO 1      /* "rho" */
+#define ZK_BD_OMEGA 2    /* "omega" */
+#define ZK_BD_PIVOT 3    /* "shadow pivot" */
+#define ZK_BD_MR 5       /* "minimal-residual basis vector {j}" */
+#define ZK_BD_SIGMA 6    /* "sigma = <r~, v>" */
+#define ZK_BD_ALPHA 7    /* "alpha" */
+#define ZK_BD_TAU 8      /* "quasi-residual tau" */
+/*                          replaces krylov.solve_bicgstab_l (krylov.py:298-410); 1 <= ell <= 32 */
+zk_status zk_bicgstab_l(zk_context* ctx, const zk_csr* A, const double* b, const double* minv,
+                        const double* x0, double tolerance, int64_t max_iterations, int ell, double* x_out,
+                        double* history_host, zk_solve_report* report, int32_t* breakdown_index);
+/*                          replaces krylov.solve_tfqmr (krylov.py:413-489) */
+zk_status zk_tfqmr(zk_context* ctx, const zk_csr* A, const double* b, const double* minv, const double* x0,
+                   double tolerance, int64_t max_iterations, double* x_out, double* history_host,
+                   zk_solve_report* report);
+
 /* ---- row-sharded BiCGStab (multi-GPU) --------------------------
  * One shard per rank (process / GPU).  The reference has no distributed
  * solver: a shard runs exactly the loop of krylov.solve_bicgstab

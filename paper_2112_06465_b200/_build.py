@@ -12,7 +12,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "lib")
 OUT = os.path.join(OUT_DIR, "libzk.so")
-SOURCES = ["zk_api.cu", "zk_blas1.cu", "zk_spmv.cu", "zk_bicgstab.cu", "zk_plan.cpp"]
+SOURCES = ["zk_api.cu", "zk_blas1.cu", "zk_spmv.cu", "zk_bicgstab.cu", "zk_krylov.cu", "zk_plan.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: no contraction anywhere -- the arithmetic must be the reference's

@@ -96,6 +96,9 @@ SIGNATURES = {
     "zk_spmv": [_vp, _vp, _vp, _vp],
     "zk_spmv_dotc": [_vp, _vp, _vp, _vp, _vp, _i, ctypes.POINTER(_d)],
     "zk_bicgstab": [_vp, _vp, _vp, _vp, _vp, _d, _i64, _vp, ctypes.POINTER(_d), ctypes.POINTER(SolveReportC)],
+    "zk_bicgstab_l": [_vp, _vp, _vp, _vp, _vp, _d, _i64, _i, _vp, ctypes.POINTER(_d), ctypes.POINTER(SolveReportC),
+                      ctypes.POINTER(ctypes.c_int32)],
+    "zk_tfqmr": [_vp, _vp, _vp, _vp, _vp, _d, _i64, _vp, ctypes.POINTER(_d), ctypes.POINTER(SolveReportC)],
     "zk_dshard_create": [_vp, _vp, _i64, _i64, _i, _i64, _i, _i64, ctypes.POINTER(_vp)],
     "zk_dshard_destroy": [_vp],
     "zk_dshard_vector": [_vp, _i, ctypes.POINTER(ctypes.POINTER(_d)), ctypes.POINTER(_i64)],

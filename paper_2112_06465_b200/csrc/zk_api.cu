@@ -95,8 +95,9 @@ void launch_zaxpy(zk_context* c, int64_t n, double2 a, const double2* x, double2
 void launch_zaxmy(zk_context* c, int64_t n, const double2* x, double2* y);
 void launch_jacobi(zk_context* c, int64_t n, const double2* v, const double2* m, double2* out);
 void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, bool conj, int64_t block, int mode,
-                 double2* result);
-void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result);
+                 double2* result, Gate gate = Gate{nullptr, 0});
+void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result,
+                   Gate gate = Gate{nullptr, 0});
 zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
                    const int64_t* ia_d, const int64_t* ja_d, const double2* aa_d);
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y);
@@ -116,6 +117,10 @@ void spmv_dot_device(zk_context* c, const zk_csr* A, const double2* x, double2* 
 int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* minv, const double2* x0, double tol,
                     int64_t maxit, double2* x_out, double* history_host, zk_solve_report* rep);
 void destroy_solver_plan(zk_context* c, SolverPlan* P);
+void destroy_krylov_plan(zk_context* c, KrylovPlan* P);
+int krylov_device(zk_context* c, zk_csr* A, int solver, int ell, const double2* b, const double2* minv,
+                  const double2* x0, double tol, int64_t maxit, double2* x_out, double* history_host,
+                  zk_solve_report* rep, int32_t* what_j);
 void destroy_sell(zk_csr* A);
 
 }  // namespace zk
@@ -581,6 +586,7 @@ zk_status zk_csr_destroy(zk_csr* A) {
         zk_context* c = A->ctx;
         cudaStreamSynchronize(c->stream);
         for (int k = 0; k < 2; ++k) destroy_solver_plan(c, A->solver[k]);
+        for (int k = 0; k < 4; ++k) destroy_krylov_plan(c, A->kplan[k]);
         destroy_sell(A);
     });
 }
@@ -653,6 +659,49 @@ zk_status zk_bicgstab(zk_context* c, const zk_csr* A, const double* b, const dou
     if (st != ZK_OK) return st;
     if (rc == ZK_ERR_BREAKDOWN) set_error("breakdown");
     return rc;
+}
+
+static zk_status krylov_entry(zk_context* c, const zk_csr* A, int solver, int ell, const double* b, const double* minv,
+                              const double* x0, double tol, int64_t maxit, double* x_out, double* history_host,
+                              zk_solve_report* rep, int32_t* breakdown_index) {
+    int rc = ZK_OK;
+    zk_status st = guarded([&] {
+        need_ctx(c);
+        need(A != nullptr, ZK_ERR_PARAMETER, "null matrix");
+        need(A->n_rows == A->n_cols, ZK_ERR_DIMENSION,
+             "matrix is " + std::to_string(A->n_rows) + "x" + std::to_string(A->n_cols) + ", not square");
+        need(tol > 0, ZK_ERR_PARAMETER, "tolerance must be positive");
+        need(maxit >= 1, ZK_ERR_PARAMETER, "max_iterations must be >= 1");
+        need(ell >= 1, ZK_ERR_PARAMETER, "polynomial degree l must be >= 1");
+        need(history_host && rep, ZK_ERR_PARAMETER, "null history/report");
+        need_ptr(b, A->n_rows, "b");
+        need_ptr(x_out, A->n_rows, "x_out");
+        std::memset(rep, 0, sizeof(*rep));
+        int32_t j = 0;
+        if (A->n_rows == 0) {  // ||b|| = 0: trivial_result (krylov.py:174-178)
+            history_host[0] = 0.0;
+            rep->converged = 1;
+            rep->history_len = 1;
+        } else {
+            rc = krylov_device(c, const_cast<zk_csr*>(A), solver, ell, D2(b), minv ? D2(minv) : nullptr,
+                               x0 ? D2(x0) : nullptr, tol, maxit, D2(x_out), history_host, rep, &j);
+        }
+        if (breakdown_index) *breakdown_index = j;
+    });
+    if (st != ZK_OK) return st;
+    if (rc == ZK_ERR_BREAKDOWN) set_error("breakdown");
+    return rc;
+}
+
+zk_status zk_bicgstab_l(zk_context* c, const zk_csr* A, const double* b, const double* minv, const double* x0,
+                        double tol, int64_t maxit, int ell, double* x_out, double* history_host,
+                        zk_solve_report* rep, int32_t* breakdown_index) {
+    return krylov_entry(c, A, 0, ell, b, minv, x0, tol, maxit, x_out, history_host, rep, breakdown_index);
+}
+
+zk_status zk_tfqmr(zk_context* c, const zk_csr* A, const double* b, const double* minv, const double* x0, double tol,
+                   int64_t maxit, double* x_out, double* history_host, zk_solve_report* rep) {
+    return krylov_entry(c, A, 1, 1, b, minv, x0, tol, maxit, x_out, history_host, rep, nullptr);
 }
 
 // ---- row-sharded BiCGStab ----------------------------------------------------

@@ -126,15 +126,17 @@ __device__ __forceinline__ void block_partial(PlanPtrs plans, int64_t n, int64_t
 __global__ void __launch_bounds__(kRedThreads, 2) k_zdot_blocks(int64_t n, int64_t nb, const double2* __restrict__ x,
                                                               const double2* __restrict__ y, bool conj, int64_t block,
                                                               PlanPtrs plans, double* slots, double2* result,
-                                                              bool fma) {
+                                                              bool fma, Gate gate) {
     extern __shared__ double2 nodes_c[];
+    if (gate.skip()) return;  // launch-uniform: every CTA returns, no slot is written
     block_partial<double2>(plans, n, nb, block, DotOp{x, y, conj, fma}, nodes_c, slots, result, false);
 }
 
 __global__ void __launch_bounds__(kRedThreads, 3) k_znorm2_blocks(int64_t n, int64_t nb, const double2* __restrict__ x,
                                                                 int64_t block, PlanPtrs plans, double* slots,
-                                                                double* result) {
+                                                                double* result, Gate gate) {
     extern __shared__ double nodes_r[];
+    if (gate.skip()) return;
     block_partial<double>(plans, n, nb, block, Norm2Op{x}, nodes_r, slots, result, true);
 }
 
@@ -210,7 +212,7 @@ double* fold_slots(zk_context* c, int64_t count) {
 }
 
 void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, bool conj, int64_t block,
-                 int mode, double2* result) {
+                 int mode, double2* result, Gate gate) {
     if (mode == ZK_MODE_SEQUENTIAL) {
         k_zdot_seq<<<1, 1, 0, c->stream>>>(n, x, y, conj, result);
         ZK_CUDA(cudaGetLastError());
@@ -227,12 +229,13 @@ void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, b
     double* slots = fold_slots(c, 2 * nb);
     if (smem > 48 * 1024)
         ZK_CUDA(cudaFuncSetAttribute(k_zdot_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_zdot_blocks<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, nb, x, y, conj, block, p, slots, result, c->fma);
+    k_zdot_blocks<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, nb, x, y, conj, block, p, slots, result, c->fma,
+                                                                  gate);
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }
 
-void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result) {
+void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result, Gate gate) {
     if (mode == ZK_MODE_SEQUENTIAL) {
         k_znorm2_seq<<<1, 1, 0, c->stream>>>(n, x, result);
         ZK_CUDA(cudaGetLastError());
@@ -249,7 +252,7 @@ void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, in
     double* slots = fold_slots(c, nb);
     if (smem > 48 * 1024)
         ZK_CUDA(cudaFuncSetAttribute(k_znorm2_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_znorm2_blocks<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, nb, x, block, p, slots, result);
+    k_znorm2_blocks<<<(unsigned)nb, kRedThreads, smem, c->stream>>>(n, nb, x, block, p, slots, result, gate);
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }

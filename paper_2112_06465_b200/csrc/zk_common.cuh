@@ -80,4 +80,23 @@ __device__ __forceinline__ bool small_py(double v) { return !(fabs(v) >= kBreakd
 
 __device__ __forceinline__ double2 ldg2(const double2* p) { return __ldg(p); }
 
+// Device-side predication of a graph-captured kernel: the solver drivers
+// capture a whole loop body once, and each kernel decides from the solver's
+// state words whether it runs (p[0] = done, p[1] = the solver's flag).
+//   kAlways: always;  kLive: unless done;  kLiveNoFlag: unless done or flag;
+//   kLiveFlag: only when not done and flag is set.
+struct Gate {
+    const int32_t* p;
+    int32_t mode;
+    enum : int32_t { kAlways = 0, kLive = 1, kLiveNoFlag = 2, kLiveFlag = 3 };
+    __device__ __forceinline__ bool skip() const {
+        if (p == nullptr || mode == kAlways) return false;
+        const int32_t done = p[0], flag = p[1];
+        if (done) return true;
+        if (mode == kLiveNoFlag) return flag != 0;
+        if (mode == kLiveFlag) return flag == 0;
+        return false;
+    }
+};
+
 }  // namespace zk

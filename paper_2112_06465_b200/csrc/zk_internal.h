@@ -53,7 +53,8 @@ private:
     std::recursive_mutex mu_;
 };
 
-struct SolverPlan;  // zk_bicgstab.cu
+struct SolverPlan;   // zk_bicgstab.cu
+struct KrylovPlan;   // zk_krylov.cu
 
 }  // namespace zk
 
@@ -76,7 +77,8 @@ struct zk_csr {
     int64_t* long_ia;               // [n_long + 1]
     int32_t* long_ja;
     double2* long_aa;
-    zk::SolverPlan* solver[2];      // [identity, jacobi]
+    zk::SolverPlan* solver[2];      // BiCGStab [identity, jacobi]
+    zk::KrylovPlan* kplan[4];       // [BiCGSTAB(l) identity, jacobi, TFQMR identity, jacobi]
 };
 
 struct zk_context {

@@ -22,7 +22,8 @@ from .errors import BreakdownError, DimensionError, ParameterError, SingularPrec
 from .sparse import CsrMatrix
 from .vecops import ZVector
 
-__all__ = ["SolverConfig", "Preconditioner", "SolveReport", "build_jacobi", "solve_bicgstab"]
+__all__ = ["SolverConfig", "Preconditioner", "SolveReport", "build_jacobi", "solve_bicgstab", "solve_bicgstab_l",
+           "solve_tfqmr"]
 
 _BREAKDOWN_EPS = 1e-300
 _BREAKDOWN_WHAT = {
@@ -129,13 +130,23 @@ class SolveReport:
     elapsed_ms: float = 0.0
 
 
-def solve_bicgstab(A, b, M=None, cfg=None):
-    """Right-preconditioned BiCGStab (van der Vorst), device-resident.
+# BreakdownError names of BiCGSTAB(l) / TFQMR (krylov.py:341-477), by ZK_BD_* code
+_EXT_BREAKDOWN_WHAT = {
+    1: "rho",
+    2: "omega",
+    3: "shadow pivot",
+    5: "minimal-residual basis vector {j}",
+    6: "sigma = <r~, v>",
+    7: "alpha",
+    8: "quasi-residual tau",
+}
 
-    Returns ``(x, SolveReport)``; non-convergence is a normal return.  Raises
-    ``BreakdownError`` (with the partial report) when rho, the shadow pivot,
-    <t,t> or omega falls below 1e-300 in magnitude.
-    """
+
+def _device_solve(entry, names, A, b, M, cfg, *extra):
+    """Shared front end of the device solvers: the reference's argument
+    checks (_Run.__init__, krylov.py:147-163), one libzk call that runs the
+    whole solve on the device, and the SolveReport / BreakdownError the
+    reference returns (krylov.py:188-206)."""
     cfg = cfg or SolverConfig()
     n = A.n
     if len(b) != n:
@@ -151,15 +162,19 @@ def solve_bicgstab(A, b, M=None, cfg=None):
     hist = (ctypes.c_double * (maxit + 1))()
     rep = _lib.SolveReportC()
     x = ZVector._device_new(n)
+    fn = getattr(_lib.lib(), entry)
+    tail = [hist, ctypes.byref(rep)]
+    index = ctypes.c_int32(0)
+    if entry == "zk_bicgstab_l":
+        tail.append(ctypes.byref(index))
     if n:
         bp = b._dptr()
         mp = M._device_minv()._dptr() if M.kind == "jacobi" else None
         gp = guess._dptr() if guess is not None else None
-        status = _lib.lib().zk_bicgstab(_lib.context(), A._device(), bp, mp, gp, float(cfg.tolerance), maxit,
-                                        x._dptr_out(), hist, ctypes.byref(rep))
+        status = fn(_lib.context(), A._device(), bp, mp, gp, float(cfg.tolerance), maxit, *extra, x._dptr_out(),
+                    *tail)
     else:
-        status = _lib.lib().zk_bicgstab(_lib.context(), A._device(), None, None, None, float(cfg.tolerance),
-                                        maxit, None, hist, ctypes.byref(rep))
+        status = fn(_lib.context(), A._device(), None, None, None, float(cfg.tolerance), maxit, *extra, None, *tail)
     if status not in (_lib.ZK_OK, _lib.ZK_ERR_BREAKDOWN):
         _lib.check(status)
     x._written()
@@ -173,8 +188,43 @@ def solve_bicgstab(A, b, M=None, cfg=None):
     )
     report.kernel_launches = int(rep.kernel_launches)  # extra attribute, not in the reference
     if status == _lib.ZK_ERR_BREAKDOWN:
-        what = _BREAKDOWN_WHAT.get(int(rep.breakdown), "recurrence")
+        what = names.get(int(rep.breakdown), "recurrence").format(j=index.value)
         raise BreakdownError(
             f"{what} numerically zero (|value| < {_BREAKDOWN_EPS:g}) after {report.iterations} iterations",
             report=report)
     return x, report
+
+
+def solve_bicgstab(A, b, M=None, cfg=None):
+    """Right-preconditioned BiCGStab (van der Vorst), device-resident
+    (krylov.py:213-295).
+
+    Returns ``(x, SolveReport)``; non-convergence is a normal return.  Raises
+    ``BreakdownError`` (with the partial report) when rho, the shadow pivot,
+    <t,t> or omega falls below 1e-300 in magnitude.
+    """
+    return _device_solve("zk_bicgstab", _BREAKDOWN_WHAT, A, b, M, cfg)
+
+
+def solve_bicgstab_l(A, b, M=None, cfg=None):
+    """Right-preconditioned BiCGSTAB(l) (Sleijpen-Fokkema), device-resident
+    (krylov.py:298-410): ``cfg.l`` BiCG steps then the degree-l
+    minimal-residual update per cycle; ``cfg.max_iterations`` caps cycles.
+
+    The whole solve is one CUDA-graph launch (csrc/zk_krylov.cu): vectors,
+    the scalar recurrences and the modified Gram-Schmidt system stay on the
+    device.  Returns and raises as :func:`solve_bicgstab`.
+    """
+    cfg = cfg or SolverConfig()
+    if cfg.l > 32:
+        raise ParameterError(f"polynomial degree l must be <= 32 on the device, got {cfg.l!r}")
+    return _device_solve("zk_bicgstab_l", _EXT_BREAKDOWN_WHAT, A, b, M, cfg, int(cfg.l))
+
+
+def solve_tfqmr(A, b, M=None, cfg=None):
+    """Right-preconditioned transpose-free QMR (Freund), device-resident
+    (krylov.py:413-489): two half-steps per iteration, each followed by the
+    true residual check.  One CUDA-graph launch per solve.  Returns and
+    raises as :func:`solve_bicgstab`.
+    """
+    return _device_solve("zk_tfqmr", _EXT_BREAKDOWN_WHAT, A, b, M, cfg)
