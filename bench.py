@@ -312,32 +312,15 @@ def run_zk(args, dist: Dist):
         Z.spmv(A, xs)
     _lib.event_record(5)
     spmv_ms = _lib.event_elapsed_ms(4, 5) / reps
-    nv = 100_000_000
-    v1 = Z.ZVector._device_new(nv)
-    v2 = Z.ZVector._device_new(nv)
-    _lib.check(_lib.lib().zk_memset(_lib.context(), v1._dptr_out(), 0, 16 * nv))
-    _lib.check(_lib.lib().zk_memset(_lib.context(), v2._dptr_out(), 0, 16 * nv))
-    Z.zdot(v1, v2)
-    _lib.event_record(6)
-    for _ in range(10):
-        Z.zdot(v1, v2)
-    _lib.event_record(7)
-    dot_ms = _lib.event_elapsed_ms(6, 7) / 10
-    _lib.event_record(8)
-    for _ in range(10):
-        Z.zaxpy(0.5 + 0.25j, v1, v2)
-    _lib.event_record(9)
-    axpy_ms = _lib.event_elapsed_ms(8, 9) / 10
-    del v1, v2, y
-
+    del y
+    sweep = blas1_sweep(peak) if not args.no_sweep else {}
+    others = {} if args.no_solvers else other_solvers(A, bv, M, B["spmv"])
     sub = {
         "zspmv_gbs": round(B["spmv"] / (spmv_ms * 1e-3) / 1e9, 1),
         "zspmv_frac": round(B["spmv"] / (spmv_ms * 1e-3) / 1e9 / peak, 3),
         "zspmv_us": round(spmv_ms * 1e3, 1),
-        "zdotc_1e8_gbs": round(32 * nv / (dot_ms * 1e-3) / 1e9, 1),
-        "zdotc_1e8_frac": round(32 * nv / (dot_ms * 1e-3) / 1e9 / peak, 3),
-        "zaxpy_1e8_gbs": round(48 * nv / (axpy_ms * 1e-3) / 1e9, 1),
-        "zaxpy_1e8_frac": round(48 * nv / (axpy_ms * 1e-3) / 1e9 / peak, 3),
+        "c2_blas1_sweep": sweep,
+        "other_solvers": others,
         "bicgstab_iteration_gbs": round(B["iteration"] / iter_s / 1e9, 1),
         "bicgstab_iteration_frac": round(B["iteration"] / iter_s / 1e9 / peak, 3),
         "bicgstab_iteration_us": round(iter_s * 1e6, 1),
@@ -498,6 +481,72 @@ def run_sharded(args, dist: Dist):
         print(json.dumps(out), flush=True)
 
 
+def other_solvers(A, bv, M, spmv_bytes, steps: int = 2):
+    """The paper's other two solvers on the same system:
+    BiCGSTAB(8) and TFQMR (krylov.py:298-489), device-resident, timed with
+    CUDA events per solve (one graph launch each) after a warm-up solve."""
+    import paper_2112_06465_b200 as Z
+    from paper_2112_06465_b200 import _lib
+    out = {}
+    for name, fn, cfg in (("bicgstab_l8", Z.solve_bicgstab_l, Z.SolverConfig(tolerance=TOL, max_iterations=MAXIT, l=8)),
+                          ("tfqmr", Z.solve_tfqmr, Z.SolverConfig(tolerance=TOL, max_iterations=MAXIT))):
+        x, rep = fn(A, bv, M, cfg)
+        l0 = Z.launch_count()
+        _lib.event_record(12)
+        for _ in range(steps):
+            x, rep = fn(A, bv, M, cfg)
+        _lib.event_record(13)
+        ms = _lib.event_elapsed_ms(12, 13) / steps
+        out[name] = {"solves_per_s": round(1e3 / ms, 4), "ms_per_solve": round(ms, 2),
+                     "iterations": rep.iterations, "converged": bool(rep.converged),
+                     "final_rel": rep.final_relative_residual,
+                     "kernels_per_solve": (Z.launch_count() - l0) // steps, "host_syncs_per_solve": 1}
+    return out
+
+
+# ---- C2: the paper's BLAS-1 study (BASELINE configs[1]) ----------------------------
+
+C2_SIZES = (10_000, 100_000, 1_000_000, 10_000_000, 100_000_000)
+C2_BYTES = {"zdotc": 32, "zaxpy": 48, "zscal": 32, "znrm2": 16}  # SURVEY 8d, per element
+
+
+def blas1_sweep(peak: float, sizes=C2_SIZES):
+    """zdotc / zaxpy / zscal / znrm2 at 1e4..1e8 complex128 elements through
+    the public API (vecops.py:124-200), inputs from random_zvector (seed 42,
+    reference bench.py:137-139).  Each timed launch is bracketed by CUDA
+    events on the library stream with a 256 MB L2 flush before it, so small
+    sizes measure HBM, not the 126 MB L2; the median of the reps is kept."""
+    import paper_2112_06465_b200 as Z
+    from paper_2112_06465_b200 import _lib
+    flush = Z.ZVector._device_new(16 * 1024 * 1024)  # 256 MB > L2
+    out = {}
+    for n in sizes:
+        rng = np.random.default_rng(42)
+        x = Z.ZVector(rng.random(n) + 1j * rng.random(n))
+        y = Z.ZVector(rng.random(n) + 1j * rng.random(n))
+        alpha = complex(rng.random(), rng.random())
+        x._dptr()
+        y._dptr()
+        ops = {"zdotc": lambda: Z.zdot(x, y), "zaxpy": lambda: Z.zaxpy(alpha, x, y),
+               "zscal": lambda: Z.zscal(alpha, x), "znrm2": lambda: Z.znorm2(x)}
+        reps = 20 if n <= 10_000_000 else 8
+        for name, fn in ops.items():
+            fn()
+            times = []
+            for _ in range(reps):
+                _lib.check(_lib.lib().zk_memset(_lib.context(), flush._dptr_out(), 1, 16 * 16 * 1024 * 1024))
+                _lib.event_record(10)
+                fn()
+                _lib.event_record(11)
+                times.append(_lib.event_elapsed_ms(10, 11))
+            ms = statistics.median(times)
+            gbs = C2_BYTES[name] * n / (ms * 1e-3) / 1e9
+            out[f"{name}_{n:.0e}".replace("+0", "")] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1),
+                                                          "frac": round(gbs / peak, 3)}
+        del x, y
+    return out
+
+
 def cpu_sample(ia, ja, aa, b, minv, iters):
     """One capped solve of the reference algorithm (oracle/port.py): setup +
     one iteration; returns (solves/s extrapolated to `iters`, detail)."""
@@ -566,6 +615,8 @@ def main():
     ap.add_argument("--impl", choices=["zk", "reference"], default="zk")
     ap.add_argument("--iterations", type=int, default=None, help="reference arm: override the committed iteration count")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the C2 BLAS-1 sweep")
+    ap.add_argument("--no-solvers", action="store_true", help="skip the BiCGSTAB(8) / TFQMR lines")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default=CONFIG, help="BASELINE system (default C4)")
     args = ap.parse_args()
     dist = Dist() if args.impl == "zk" else _NoDist()
