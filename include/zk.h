@@ -117,6 +117,14 @@ zk_status zk_zdotc(zk_context* ctx, int64_t n, const double* x, const double* y,
 zk_status zk_znorm2(zk_context* ctx, int64_t n, const double* x, int64_t block_size, int mode,
                     double* result_host);
 
+/* Same reductions, asynchronous: the result lands in device memory
+ * (result_dev: 2 doubles for zdotc, 1 for znorm2), stream-ordered, no host
+ * wait -- for device-resident pipelines (and kernel-only timing). */
+zk_status zk_zdotc_dev(zk_context* ctx, int64_t n, const double* x, const double* y, int conjugate,
+                       int64_t block_size, int mode, double* result_dev);
+zk_status zk_znorm2_dev(zk_context* ctx, int64_t n, const double* x, int64_t block_size, int mode,
+                        double* result_dev);
+
 /* ---- CSR matrix and SpMV (sparse.py) ------------------------------------ */
 /* Upload a validated CSR (zero-based int64 ia[n_rows+1], ja[nnz]; complex128
  * aa[nnz]; strictly increasing columns per row -- CsrMatrix._validate,

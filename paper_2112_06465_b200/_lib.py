@@ -89,6 +89,8 @@ SIGNATURES = {
     "zk_jacobi_apply": [_vp, _i64, _vp, _vp, _vp],
     "zk_zdotc": [_vp, _i64, _vp, _vp, _i, _i64, _i, ctypes.POINTER(_d)],
     "zk_znorm2": [_vp, _i64, _vp, _i64, _i, ctypes.POINTER(_d)],
+    "zk_zdotc_dev": [_vp, _i64, _vp, _vp, _i, _i64, _i, _vp],
+    "zk_znorm2_dev": [_vp, _i64, _vp, _i64, _i, _vp],
     "zk_csr_create": [_vp, _i64, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)],
     "zk_csr_create_device": [_vp, _i64, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_vp)],
     "zk_csr_destroy": [_vp],

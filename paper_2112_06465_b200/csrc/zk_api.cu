@@ -141,6 +141,15 @@ char* zk_context::plan(int32_t L, int32_t kind) {
     return d;
 }
 
+const char* zk_context::plan_host(int32_t L, int32_t kind) {
+    auto key = std::make_pair(L, kind);
+    auto it = plans_h.find(key);
+    if (it != plans_h.end()) return it->second.data();
+    std::vector<char> host(build_plan(L, kind, nullptr));
+    build_plan(L, kind, host.data());
+    return plans_h.emplace(key, std::move(host)).first->second.data();
+}
+
 PlanPtrs zk_context::plans_for(int64_t n, int64_t block, int32_t kind) {
     PlanPtrs p;
     p.full = plan((int32_t)(block - 1), kind);
@@ -504,6 +513,38 @@ zk_status zk_zdotc(zk_context* c, int64_t n, const double* x, const double* y, i
         ZK_CUDA(cudaStreamSynchronize(c->stream));
         result_host[0] = c->h_result[0];
         result_host[1] = c->h_result[1];
+    });
+}
+
+zk_status zk_zdotc_dev(zk_context* c, int64_t n, const double* x, const double* y, int conjugate, int64_t block_size,
+                       int mode, double* result_dev) {
+    return guarded([&] {
+        need_ctx(c);
+        check_plan(block_size, mode);
+        need(n >= 0, ZK_ERR_DIMENSION, "negative length");
+        need(result_dev != nullptr, ZK_ERR_PARAMETER, "null result");
+        if (n == 0) {
+            ZK_CUDA(cudaMemsetAsync(result_dev, 0, sizeof(double2), c->stream));
+            return;
+        }
+        need_ptr(x, n, "x");
+        need_ptr(y, n, "y");
+        zdot_device(c, n, D2(x), D2(y), conjugate != 0, block_size, mode, reinterpret_cast<double2*>(result_dev));
+    });
+}
+
+zk_status zk_znorm2_dev(zk_context* c, int64_t n, const double* x, int64_t block_size, int mode, double* result_dev) {
+    return guarded([&] {
+        need_ctx(c);
+        check_plan(block_size, mode);
+        need(n >= 0, ZK_ERR_DIMENSION, "negative length");
+        need(result_dev != nullptr, ZK_ERR_PARAMETER, "null result");
+        if (n == 0) {
+            ZK_CUDA(cudaMemsetAsync(result_dev, 0, sizeof(double), c->stream));
+            return;
+        }
+        need_ptr(x, n, "x");
+        znorm2_device(c, n, D2(x), block_size, mode, result_dev);
     });
 }
 

@@ -18,6 +18,10 @@
 // SpMV phases are persistent TMA-pipelined kernels (zk_spmv.cuh); the
 // reduction of each 4096-row block runs on the consumer warps as soon as the
 // block's rows are done, while the producer warp keeps streaming the matrix.
+// The level-1 phases K3 and K5 run on the TMA-fed block-reduction engine
+// (zk_l1pipe.cuh): their input vectors stream into shared memory stage by
+// stage (one pairwise subtree per stage) and consumer warps apply the fused
+// updates and the numpy-order sums from there.
 // The CTA that finishes the last block folds the block partials in order
 // and runs the scalar recurrences (Python Cplx arithmetic, zk_common.cuh) on
 // a device SolverState.  The loop is a CUDA-graph conditional WHILE node
@@ -28,11 +32,14 @@
 
 #include "zk_internal.h"
 #include "zk_blockred.cuh"
+#include "zk_l1pipe.cuh"
 #include "zk_spmv.cuh"
 
 namespace zk {
 
 SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv);
+bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
+             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid);
 size_t pipe_smem_bytes(const SellView& v, size_t extra);
 unsigned pipe_grid(const zk_csr* A);
 
@@ -59,10 +66,6 @@ struct SolverBufs {
     int dist;          // row-sharded solve: block partials are folded across ranks (k_fold_finish)
 };
 
-constexpr int kNodesPerBuf = 2 * 136;             // node slots per buffer (<= 129 nodes x NACC 2)
-constexpr int kNodeBytes = 2 * kNodesPerBuf * 16;  // double-buffered plan nodes
-constexpr int kRedThreads = 288;                   // 65 complex leaves x 4 lanes fit one pass
-constexpr int kEwSmem = kNodeBytes;
 
 struct SolverPlan {
     int64_t n = 0;
@@ -305,98 +308,7 @@ __global__ void k_fill_empty(double* p, int64_t n) {
         p[i] = __longlong_as_double((long long)kSlotEmpty);
 }
 
-// ---- persistent block-pass kernels for the fused level-1 phases ----------
-// One CTA loops over blocks; per block: leaf phase (all threads, operands
-// prefetched in registers), one CTA barrier, then warp 0 combines the tree
-// while the other warps start the next block.  Nodes are double-buffered.
-// STREAM (1 GPU): CTA 0 is the folder -- its warp 0 folds the partials in
-// block order while CTAs 1.. produce them (stream_fold, no per-block fence
-// or atomic) and runs the phase's scalar recurrences (fin.finish), so the
-// serial fold (~17 cycles per partial) overlaps the pass instead of
-// following it.  !STREAM (row-sharded solve): the partials are stored for
-// the cross-rank gather and k_fold_finish folds them in global order.
-// The folder warp's work, out of line so it does not add to the workers'
-// register allocation.
-template <int NP, class Fin>
-__device__ __noinline__ void fold_and_finish(double* slots, int64_t nblocks, Fin fin) {
-    double t[NP];
-    stream_fold<NP>(slots, nblocks, t);
-    if (threadIdx.x == 0) fin.finish(t);
-}
-
-template <bool STREAM, typename V, int NACC, class Op, class Fin>
-__device__ __forceinline__ void persistent_blocks(PlanPtrs plans, int64_t n, int64_t nblocks, const Op& op,
-                                                  V* nodes, double* partials, double* slots, Fin fin) {
-    constexpr int NP = NACC * (int)(sizeof(V) / sizeof(double));
-    static_assert(NP == Fin::kNP, "partials per block");
-    int64_t first = blockIdx.x, stride = gridDim.x;
-    if constexpr (STREAM) {
-        if (blockIdx.x == 0) {
-            if (threadIdx.x < 32) fold_and_finish<NP>(slots, nblocks, fin);
-            return;
-        }
-        first -= 1;
-        stride -= 1;
-    }
-    double* out = STREAM ? slots : partials;
-    int buf = 0;
-    for (int64_t blk = first; blk < nblocks; blk += stride) {
-        const int64_t base = blk * kBlock;
-        const char* plan = (base + kBlock <= n) ? plans.full : plans.tail;
-        V* nb = nodes + buf * kNodesPerBuf;
-        V v0[NACC];
-        if (threadIdx.x == 0) {
-            typename Op::Item it = op.load(base);
-            op.apply(base, it, v0);
-        }
-        leaf_phase<V, NACC>(plan, base + 1, op, nb, blockDim.x);
-        __syncthreads();
-        buf ^= 1;
-        if ((threadIdx.x >> 5) != 0) continue;
-        V pw[NACC];
-        warp_tree<V, NACC>(plan, nb, pw);
-        if ((threadIdx.x & 31) == 0) {
-            const bool has = plan_hdr(plan)->L > 0;
-#pragma unroll
-            for (int a = 0; a < NACC; ++a) {
-                const V p = has ? VT<V>::add(v0[a], pw[a]) : v0[a];
-                const double* pd = reinterpret_cast<const double*>(&p);
-#pragma unroll
-                for (int c = 0; c < NP / NACC; ++c) {
-                    if constexpr (STREAM) slot_store(out + (blk * NACC + a) * (NP / NACC) + c, pd[c]);
-                    else out[(blk * NACC + a) * (NP / NACC) + c] = pd[c];
-                }
-            }
-        }
-    }
-}
-
 // ---- K3: s = r + F1(-alpha, v); s^ = M s; ||s|| -> s-check (krylov.py:272-275) ----
-struct SUpdateOp {
-    const double2* r;
-    const double2* v;
-    const double2* minv;
-    double2* s;
-    double2* sh;
-    double2 ma;
-    bool jacobi, fma;
-    struct Item { double2 r, v, m; };
-    static constexpr int U = 2;
-    __device__ Item load(int64_t e) const {
-        Item it;
-        it.r = r[e];
-        it.v = v[e];
-        if (jacobi) it.m = __ldg(minv + e);
-        return it;
-    }
-    __device__ void apply(int64_t e, const Item& it, double (&out)[1]) const {
-        double2 sv = cadd(it.r, f1(ma, it.v, fma));
-        s[e] = sv;
-        if (jacobi) sh[e] = f1(sv, it.m, fma);
-        out[0] = abs2_np(sv);
-    }
-};
-
 // s-check decision from the folded ||s||^2 (krylov.py:275)
 struct SUpdFinish {
     static constexpr int kNP = 1;
@@ -408,15 +320,30 @@ struct SUpdFinish {
     }
 };
 
-template <bool STREAM>
-__global__ void __launch_bounds__(kRedThreads, 2) k_s_update(SolverBufs B, PlanPtrs pr) {
+// K3 on the TMA-fed engine (zk_l1pipe.cuh): staged r, v, minv
+struct SUpdPipeOp {
+    using V = double;
+    static constexpr int NIN = 3;
+    double2* s;
+    double2* sh;
+    double2 ma;
+    bool jacobi, fma;
+    __device__ __forceinline__ double apply(int64_t e, const double2 (&v)[3]) const {
+        const double2 sv = cadd(v[0], f1(ma, v[1], fma));
+        s[e] = sv;
+        if (jacobi) sh[e] = f1(sv, v[2], fma);
+        return abs2_np(sv);
+    }
+};
+
+__global__ void __launch_bounds__(kL1Threads, 1) k_s_update_pipe(SolverBufs B, L1View P) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
     if (blockIdx.x == 0 && threadIdx.x == 0) st->trips++;  // loop-body executions (launch accounting)
     if (st->done) return;
-    SUpdateOp op{B.r, B.v, B.minv, B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
-    persistent_blocks<STREAM, double, 1>(pr, B.n, B.nblocks, op, reinterpret_cast<double*>(smem), B.partials,
-                                         B.slots, SUpdFinish{B});
+    SUpdPipeOp op{B.s, B.sh, neg(st->alpha), B.jacobi, B.fma};
+    SUpdFinish fin{B};
+    l1_pipeline(P, op, fin, smem);
 }
 
 // ---- K3x: x = x + F1(alpha, p^), only on the s-check path (krylov.py:274) ----
@@ -431,39 +358,6 @@ __global__ void __launch_bounds__(256) k_x_alpha(SolverBufs B) {
 }
 
 // ---- K5: x, r updates and <r~, r> -> rho', beta (krylov.py:288-290, 255-261) ----
-struct XrOp {
-    double2* x;
-    double2* r;
-    const double2* ph;
-    const double2* sh;
-    const double2* s;
-    const double2* t;
-    const double2* rs;
-    double2 a, w, mw;
-    bool applied, fma;
-    struct Item { double2 x, ph, sh, s, t, rs; };
-    static constexpr int U = 1;
-    __device__ Item load(int64_t e) const {
-        Item it;
-        it.x = x[e];
-        if (!applied) it.ph = ph[e];
-        it.sh = sh[e];
-        it.s = s[e];
-        it.t = t[e];
-        it.rs = __ldg(rs + e);
-        return it;
-    }
-    __device__ void apply(int64_t e, const Item& it, double2 (&v)[1]) const {
-        double2 xv = it.x;
-        if (!applied) xv = cadd(xv, f1(a, it.ph, fma));
-        xv = cadd(xv, f1(w, it.sh, fma));
-        x[e] = xv;
-        double2 rv = cadd(it.s, f1(mw, it.t, fma));
-        r[e] = rv;
-        v[0] = f1(conjz(it.rs), rv, fma);
-    }
-};
-
 // rho' = <r~, r> -> rho, beta of the next iteration (krylov.py:255-261)
 struct XrFinish {
     static constexpr int kNP = 2;
@@ -481,15 +375,34 @@ struct XrFinish {
     }
 };
 
-template <bool STREAM>
-__global__ void __launch_bounds__(kRedThreads, 2) k_xr_update(SolverBufs B, PlanPtrs pc) {
+// K5 on the TMA-fed engine: staged x, p^, s^, s, t, r~ (p^ is staged even when
+// the s-check path already applied alpha p^: that path runs at most once)
+struct XrPipeOp {
+    using V = double2;
+    static constexpr int NIN = 6;
+    double2* x;
+    double2* r;
+    double2 a, w, mw;
+    bool applied, fma;
+    __device__ __forceinline__ double2 apply(int64_t e, const double2 (&v)[6]) const {
+        double2 xv = v[0];
+        if (!applied) xv = cadd(xv, f1(a, v[1], fma));
+        xv = cadd(xv, f1(w, v[2], fma));
+        x[e] = xv;
+        const double2 rv = cadd(v[3], f1(mw, v[4], fma));
+        r[e] = rv;
+        return f1(conjz(v[5]), rv, fma);
+    }
+};
+
+__global__ void __launch_bounds__(kL1Threads, 1) k_xr_update_pipe(SolverBufs B, L1View P) {
     extern __shared__ __align__(128) unsigned char smem[];
     SolverState* st = B.st;
     if (st->done) return;
     const double2 a = st->alpha, w = st->omega;
-    XrOp op{B.x, B.r, B.ph, B.sh, B.s, B.t, B.rs, a, w, neg(w), st->alpha_applied != 0, B.fma};
-    persistent_blocks<STREAM, double2, 1>(pc, B.n, B.nblocks, op, reinterpret_cast<double2*>(smem), B.partials,
-                                          B.slots, XrFinish{B});
+    XrPipeOp op{B.x, B.r, a, w, neg(w), st->alpha_applied != 0, B.fma};
+    XrFinish fin{B};
+    l1_pipeline(P, op, fin, smem);
 }
 
 // ---- ordered fold of block partials + the phase's scalar recurrences ----------
@@ -541,9 +454,12 @@ struct Launch {
     size_t smem_s, smem_p, smem_t, smem_r;
     RedCfg red;
     PlanPtrs pc, pr;
-    unsigned nb, ew, pg, rg;  // blocks, elementwise grid, SpMV grid, level-1 persistent grid
-    unsigned rs;              // streaming level-1 grid: folder CTA + workers
+    unsigned nb, ew, pg;      // blocks, elementwise grid, SpMV grid
     RankCounts one;           // {nblocks}: the 1-GPU fold's partial count
+    // K3 / K5 on the TMA-fed engine (zk_l1pipe.cuh)
+    L1View l1s, l1x;
+    size_t smem_l1s = 0, smem_l1x = 0;
+    unsigned grid_l1s = 0, grid_l1x = 0;
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
@@ -572,7 +488,7 @@ constexpr int kPrologueKernels = 3;
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
     if (pe) pe->rec(3, s);
-    k_s_update<true><<<L.rs, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pr);
+    k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(L.P->bufs, L.l1s);
     if (pe) pe->rec(4, s);
     k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
     if (pe) pe->rec(5, s);
@@ -580,7 +496,7 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     if (pe) pe->rec(6, s);
     k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.red);
     if (pe) pe->rec(7, s);
-    k_xr_update<true><<<L.rs, kRedThreads, kEwSmem, s>>>(L.P->bufs, L.pc);
+    k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(L.P->bufs, L.l1x);
     if (pe) pe->rec(8, s);
     k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
     if (pe) pe->rec(9, s);
@@ -608,10 +524,8 @@ void set_attrs(const Launch& L) {
     smem_attr(k_spmv_t, L.smem_t);
     smem_attr(k_true_res<0>, L.smem_r);
     smem_attr(k_true_res<1>, L.smem_r);
-    smem_attr(k_s_update<true>, kEwSmem);
-    smem_attr(k_xr_update<true>, kEwSmem);
-    smem_attr(k_s_update<false>, kEwSmem);
-    smem_attr(k_xr_update<false>, kEwSmem);
+    smem_attr(k_s_update_pipe, L.smem_l1s);
+    smem_attr(k_xr_update_pipe, L.smem_l1x);
 }
 
 bool use_graph() {
@@ -730,11 +644,21 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.one = RankCounts{};
     L.one.n[0] = B.nblocks;
     L.pg = pipe_grid(A);
-    L.rg = (unsigned)(B.nblocks < 2 * num_sms() ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms());
-    L.rs = 1 + (unsigned)(B.nblocks < 2 * num_sms() - 1 ? (B.nblocks > 0 ? B.nblocks : 1) : 2 * num_sms() - 1);
     int64_t ewg = (n + 255) / 256;
     int64_t cap = (int64_t)num_sms() * 8;
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
+    {
+        double* slots = B.dist ? nullptr : B.slots;
+        double* partials = B.dist ? B.partials : nullptr;
+        // K3 stages r, v (and minv); K5 x, p^, s^ (identity: s^ is s), s, t, r~
+        const double2* in3[3] = {B.r, B.v, B.jacobi ? B.minv : nullptr};
+        const int8_t al3[3] = {0, 0, 0};
+        const double2* in5[6] = {B.x, B.ph, B.jacobi ? B.sh : nullptr, B.s, B.t, B.rs};
+        const int8_t al5[6] = {0, 0, 3, 0, 0, 0};
+        if (n > 0 && (!l1_view(c, n, kReal, in3, al3, 3, slots, partials, L.l1s, L.smem_l1s, L.grid_l1s) ||
+                      !l1_view(c, n, kComplex, in5, al5, 6, slots, partials, L.l1x, L.smem_l1x, L.grid_l1x)))
+            throw ZkError{ZK_ERR_CUDA, "level-1 engine geometry"};
+    }
     set_attrs(L);
     return L;
 }
@@ -923,11 +847,11 @@ void dist_phase(DistSolver* D, int phase) {
         case ZK_DPHASE_SETUP: k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); break;
         case ZK_DPHASE_P_FIRST: k_p_first<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_PIVOT: k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, B, L.red, 0, 0); break;
-        case ZK_DPHASE_S_UPDATE: k_s_update<false><<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pr); break;
+        case ZK_DPHASE_S_UPDATE: k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s); break;
         case ZK_DPHASE_X_ALPHA: k_x_alpha<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_TRUE_RES_S: k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_SPMV_T: k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, B, L.red); break;
-        case ZK_DPHASE_XR_UPDATE: k_xr_update<false><<<L.rg, kRedThreads, kEwSmem, s>>>(B, L.pc); break;
+        case ZK_DPHASE_XR_UPDATE: k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); break;
         case ZK_DPHASE_TRUE_RES: k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_P_NEXT: k_p_next<<<L.ew, 256, 0, s>>>(B); break;
         default: throw ZkError{ZK_ERR_PARAMETER, "unknown solver phase"};

@@ -4,8 +4,11 @@
 // (16-byte, coalesced) with 4 independent elements per thread in flight.
 // Reductions run one CTA per ReductionPlan block (numpy's pairwise order,
 // zk_blockred.cuh) and a one-warp kernel folds the block partials in order.
+#include <cstring>
+
 #include "zk_internal.h"
 #include "zk_blockred.cuh"
+#include "zk_l1pipe.cuh"
 
 namespace zk {
 
@@ -140,6 +143,48 @@ __global__ void __launch_bounds__(kRedThreads, 3) k_znorm2_blocks(int64_t n, int
     block_partial<double>(plans, n, nb, block, Norm2Op{x}, nodes_r, slots, result, true);
 }
 
+// ---- DEFAULT_PLAN (4096) reductions on the TMA-fed engine (zk_l1pipe.cuh) ----
+struct DotPipeOp {
+    using V = double2;
+    static constexpr int NIN = 2;
+    bool conj, fma;
+    __device__ __forceinline__ double2 apply(int64_t, const double2 (&v)[2]) const {
+        double2 a = v[0];
+        if (conj) a.y = -a.y;  // np.conj
+        return f1(a, v[1], fma);
+    }
+};
+
+struct NormPipeOp {
+    using V = double;
+    static constexpr int NIN = 1;
+    __device__ __forceinline__ double apply(int64_t, const double2 (&v)[1]) const { return abs2_np(v[0]); }
+};
+
+struct DotFin {
+    static constexpr int kNP = 2;
+    double2* result;
+    __device__ void finish(const double* t) { *result = make_double2(t[0], t[1]); }
+};
+
+struct NormFin {
+    static constexpr int kNP = 1;
+    double* result;
+    __device__ void finish(const double* t) { *result = __dsqrt_rn(t[0]); }
+};
+
+__global__ void __launch_bounds__(kL1Threads, 1) k_zdot_pipe(L1View P, DotPipeOp op, DotFin fin, Gate gate) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (gate.skip()) return;
+    l1_pipeline(P, op, fin, smem);
+}
+
+__global__ void __launch_bounds__(kL1Threads, 1) k_znorm2_pipe(L1View P, NormPipeOp op, NormFin fin, Gate gate) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (gate.skip()) return;
+    l1_pipeline(P, op, fin, smem);
+}
+
 __global__ void k_fill_empty(double* slots, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         slots[i] = __longlong_as_double((long long)kSlotEmpty);
@@ -211,8 +256,61 @@ double* fold_slots(zk_context* c, int64_t count) {
     return c->slots;
 }
 
+// Engine geometry for a DEFAULT_PLAN pass over n elements with the given
+// staged inputs; false when the plans do not fit the engine (tail block with
+// more stages than a full one), so the caller takes the block-per-CTA path.
+bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
+             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid) {
+    if (n <= 0) return false;
+    const PlanPtrs p = c->plans_for(n, kBlock, kind);
+    const PlanHeader* hf = reinterpret_cast<const PlanHeader*>(c->plan_host(kBlock - 1, kind));
+    const int64_t nb = (n + kBlock - 1) / kBlock;
+    const int32_t tail_len = (int32_t)(n - (nb - 1) * kBlock) - 1;
+    const PlanHeader* ht = reinterpret_cast<const PlanHeader*>(c->plan_host(tail_len, kind));
+    if (ht->nstages > hf->nstages) return false;
+    std::memset(&P, 0, sizeof(P));
+    P.n = n;
+    P.nblocks = nb;
+    P.plans = p;
+    int staged = 0;
+    for (int v = 0; v < nin_op; ++v) {
+        P.in[v] = in[v];
+        P.alias[v] = alias ? alias[v] : 0;
+        if (in[v]) ++staged;
+    }
+    P.nin = staged;
+    P.slot_bytes = staged * kStageMaxElems * 16;
+    const size_t head = kind == kComplex ? L1Smem<double2>::kHead : L1Smem<double>::kHead;
+    const size_t limit = 227 * 1024 - kL1StaticSmem;
+    int ns = (int)((limit - head) / (size_t)P.slot_bytes);
+    if (ns > L1Smem<double>::kMaxSlots) ns = L1Smem<double>::kMaxSlots;
+    if (ns < 2) return false;
+    P.ns = ns;
+    P.slots = slots;
+    P.partials = partials;
+    smem = head + (size_t)ns * P.slot_bytes;
+    const int64_t g = nb < num_sms() ? nb : num_sms();
+    grid = (unsigned)g;
+    return true;
+}
+
 void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, bool conj, int64_t block,
                  int mode, double2* result, Gate gate) {
+    if (mode == ZK_MODE_BLOCKED && block == kBlock) {
+        const int64_t nb = (n + kBlock - 1) / kBlock;
+        const double2* in[2] = {x, x == y ? nullptr : y};
+        const int8_t alias[2] = {0, 0};
+        L1View P;
+        size_t smem;
+        unsigned grid;
+        if (l1_view(c, n, kComplex, in, alias, 2, fold_slots(c, 2 * nb), nullptr, P, smem, grid)) {
+            ZK_CUDA(cudaFuncSetAttribute(k_zdot_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_zdot_pipe<<<grid, kL1Threads, smem, c->stream>>>(P, DotPipeOp{conj, c->fma != 0}, DotFin{result}, gate);
+            ZK_CUDA(cudaGetLastError());
+            c->launches++;
+            return;
+        }
+    }
     if (mode == ZK_MODE_SEQUENTIAL) {
         k_zdot_seq<<<1, 1, 0, c->stream>>>(n, x, y, conj, result);
         ZK_CUDA(cudaGetLastError());
@@ -236,6 +334,20 @@ void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, b
 }
 
 void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result, Gate gate) {
+    if (mode == ZK_MODE_BLOCKED && block == kBlock) {
+        const int64_t nb = (n + kBlock - 1) / kBlock;
+        const double2* in[1] = {x};
+        L1View P;
+        size_t smem;
+        unsigned grid;
+        if (l1_view(c, n, kReal, in, nullptr, 1, fold_slots(c, nb), nullptr, P, smem, grid)) {
+            ZK_CUDA(cudaFuncSetAttribute(k_znorm2_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_znorm2_pipe<<<grid, kL1Threads, smem, c->stream>>>(P, NormPipeOp{}, NormFin{result}, gate);
+            ZK_CUDA(cudaGetLastError());
+            c->launches++;
+            return;
+        }
+    }
     if (mode == ZK_MODE_SEQUENTIAL) {
         k_znorm2_seq<<<1, 1, 0, c->stream>>>(n, x, result);
         ZK_CUDA(cudaGetLastError());

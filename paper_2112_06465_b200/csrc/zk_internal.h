@@ -104,6 +104,8 @@ struct zk_context {
     std::mutex mu;
 
     char* plan(int32_t L, int32_t kind);
+    const char* plan_host(int32_t L, int32_t kind);       // host copy of the same plan
+    std::map<std::pair<int32_t, int32_t>, std::vector<char>> plans_h;
     zk::PlanPtrs plans_for(int64_t n, int64_t block, int32_t kind);
     void* scratch_partials(size_t bytes);
     // streaming-fold slots (zk_blas1.cu): kept filled with the empty marker

@@ -93,11 +93,51 @@ size_t build_plan(int32_t L, int32_t kind, void* out) {
         while (k < nleaves && 1 + B.leaf_start[k] + B.leaf_len[k] <= 32 * j) ++k;
         h.leaf_upto[j] = (int16_t)k;
     }
+    // stages: subtrees of the same recursion with <= kStageItems / lanes leaves
+    std::vector<int32_t> stages;  // (b_lo, b_hi, l_lo, l_hi)
+    {
+        const int32_t maxl = kStageItems / B.lanes;
+        auto first_leaf = [&](int32_t pos) {  // first leaf starting at or after pos
+            return (int32_t)(std::lower_bound(B.leaf_start.begin(), B.leaf_start.end(), pos) - B.leaf_start.begin());
+        };
+        std::vector<std::pair<int32_t, int32_t>> todo;  // explicit stack of (s, L), leftmost first
+        if (L > 0 && !seq) todo.push_back({0, L});
+        std::vector<std::pair<int32_t, int32_t>> ranges;
+        while (!todo.empty()) {
+            auto [s0, l0] = todo.back();
+            todo.pop_back();
+            const int32_t lo = first_leaf(s0), hi = first_leaf(s0 + l0);
+            if (hi - lo <= maxl) {
+                ranges.push_back({s0, l0});
+                continue;
+            }
+            int32_t hh;
+            if (B.lanes == 4) {
+                hh = (l0 - l0 % 8) / 2;
+            } else {
+                hh = l0 / 2;
+                hh -= hh % 8;
+            }
+            todo.push_back({s0 + hh, l0 - hh});  // right pushed first: left is processed first
+            todo.push_back({s0, hh});
+        }
+        if (ranges.empty()) {  // L == 0 (head only) or a sequential leaf
+            stages.insert(stages.end(), {0, 1 + std::max(L, 0), 0, nleaves});
+        } else {
+            for (size_t k = 0; k < ranges.size(); ++k) {
+                const int32_t s0 = ranges[k].first, l0 = ranges[k].second;
+                stages.insert(stages.end(), {k == 0 ? 0 : 1 + s0, 1 + s0 + l0, first_leaf(s0), first_leaf(s0 + l0)});
+            }
+        }
+    }
+    h.nstages = (int32_t)(stages.size() / 4);
     size_t leaves_bytes = sizeof(int32_t) * 2 * (size_t)nleaves;
     size_t ops_bytes = sizeof(int32_t) * 4 * (size_t)cnt;
+    size_t stages_bytes = sizeof(int32_t) * stages.size();
     h.leaves_off = (int32_t)((sizeof(PlanHeader) + 15) / 16 * 16);
     h.ops_off = (int32_t)((h.leaves_off + leaves_bytes + 15) / 16 * 16);
-    size_t total = (h.ops_off + ops_bytes + 15) / 16 * 16;
+    h.stages_off = (int32_t)((h.ops_off + ops_bytes + 15) / 16 * 16);
+    size_t total = (h.stages_off + stages_bytes + 15) / 16 * 16;
     if (out) {
         char* o = static_cast<char*>(out);
         std::memset(o, 0, total);
@@ -108,6 +148,7 @@ size_t build_plan(int32_t L, int32_t kind, void* out) {
             lv[2 * i + 1] = B.leaf_len[i];
         }
         if (cnt) std::memcpy(o + h.ops_off, ops.data(), ops_bytes);
+        std::memcpy(o + h.stages_off, stages.data(), stages_bytes);
     }
     return total;
 }

@@ -33,12 +33,22 @@ struct PlanHeader {
     int32_t leaves_off;     // int2 (start, len) array, byte offset from header
     int32_t ops_off;        // int4 (dst, a, b, 0) array, byte offset from header
     int32_t nops;
-    int32_t pad;
+    // Stage table (int4 {b_lo, b_hi, l_lo, l_hi} at stages_off): the segment
+    // cut into subtrees of the pairwise recursion with at most 32 (leaf,
+    // lane) items each -- 8 complex / 4 real leaves, <= 512 elements --
+    // stage s holding block elements [b_lo, b_hi) (stage 0 also element 0,
+    // the reduceat head) and leaves [l_lo, l_hi).  The TMA-fed level-1
+    // engine (zk_l1pipe.cuh) streams a block stage by stage.
+    int32_t nstages;
+    int32_t stages_off;
     // leaf_upto[j]: number of leaves whose elements all lie in rows [0, 32*j)
     // of the 4096-row block (element e of the segment is block row 1+e); lets
     // the SpMV kernels reduce leaves as soon as the rows under them are done.
     int16_t leaf_upto[130];
 };
+
+constexpr int kStageItems = 32;     // (leaf, lane) items per stage: one warp
+constexpr int kStageMaxElems = 520; // >= 1 + 8 * 64 (complex) and 1 + 4 * 128 (real)
 
 // Builds the plan for segment length L into `out` (host memory); returns the
 // number of bytes used.  `out` may be null to query the size.
