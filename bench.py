@@ -187,26 +187,34 @@ def algorithmic_bytes(n: int, nnz: int):
     Ar = 20 * nnz + 4 * (n + 1)  # matrix stream only
     return {
         "spmv": A,
-        "spmv_pivot": A + 16 * n,             # + r~ read for <r~, v>
-        "pivot_first": A + 16 * n,
-        "spmv_t": A + 16 * n,                 # + s read for <t, s>
-        "true_res": Ar + 32 * n,             # A, x, b
+        "spmv_pivot": A,                      # v = A p^ (plain pipeline)
+        "pivot_first": A,
+        "pivot_dot": 32 * n,                  # <r~, v>: r~, v
+        "pivot_first_dot": 32 * n,
+        "spmv_t": A,                          # t = A s^
+        "tt_ts": 32 * n,                      # <t, t>, <t, s>: t, s
+        "true_res": Ar + 32 * n,              # A, x, b
         "p_next": 96 * n,                     # p, v, r, minv -> p, p^
         "true_res_s": Ar + 32 * n,
         "s_update": 80 * n,
         "xr_update": 128 * n,
         "x_alpha": 48 * n,
         "p_first": 96 * n,
+        # the minimum of SURVEY 8d (the <r~,v> and <t,s> operands counted with
+        # their SpMV); the two reduction passes re-read v and t (+32n)
         "iteration": 3 * A + 336 * n,
     }
 
 
-def traffic_from_profiles(kernel: str):
-    """dram bytes per launch for `kernel` from the committed ncu summary."""
+def traffic_from_profiles(kernel: str, config: str = CONFIG):
+    """DRAM bytes (read + write) per launch of `kernel` on `config`, from the
+    committed ncu capture of the current build (profiles/traffic.json:
+    {"build": ..., "<config>": {"<kernel>": bytes}}); None when that
+    configuration or kernel was not captured."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(kernel)
+            return json.load(fh).get(config, {}).get(kernel)
     except Exception:  # noqa: BLE001
         return None
 
@@ -284,22 +292,35 @@ def run_zk(args, dist: Dist):
     _lib.profile_enable(False)
     B = algorithmic_bytes(n, nnz)
     phases = {}
+    conditional = ("x_alpha", "true_res_s")  # device no-ops unless the s-check fires: no bytes credited
     for name, (tms, cnt) in prof.items():
         if cnt:
             avg = tms / cnt
             entry = {"launches": cnt, "avg_us": round(avg * 1e3, 2), "total_ms": round(tms, 3)}
-            if name in B:
+            if name in B and name not in conditional:
                 entry["gbs"] = round(B[name] / (avg * 1e-3) / 1e9, 1)
             phases[name] = entry
-    body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update", "true_res", "p_next",
-                        "spmv_pivot")
+    body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "tt_ts", "xr_update", "true_res", "p_next",
+                        "spmv_pivot", "pivot_dot")
             if p in phases]
-    dominant = max(body, key=lambda p: phases[p]["total_ms"])
-    dom_avg_s = prof[dominant][0] / prof[dominant][1] / 1e3
-    achieved = B[dominant] / dom_avg_s / 1e9
+    kernel_names = {"spmv_pivot": "k_spmv_phase", "spmv_t": "k_spmv_phase", "true_res": "k_true_res<1>",
+                    "s_update": "k_s_update_pipe", "xr_update": "k_xr_update_pipe", "tt_ts": "k_tt_ts_pass",
+                    "pivot_dot": "k_pivot_pass", "p_next": "k_p_next"}
+    # dominant kernel = the most device time per solve, summed over the
+    # phases it runs (k_spmv_phase serves both the K2 and K4 products)
+    per_kernel = {}
+    for p in body:
+        if p in conditional:
+            continue
+        k = kernel_names.get(p, p)
+        t, c_, b = per_kernel.get(k, (0.0, 0, 0))
+        per_kernel[k] = (t + prof[p][0], c_ + prof[p][1], b + B[p] * prof[p][1])
+    dominant = max(per_kernel, key=lambda k: per_kernel[k][0])
+    dom_ms, dom_cnt, dom_bytes = per_kernel[dominant]
+    dom_avg_s = dom_ms / dom_cnt / 1e3
+    dom_bytes_launch = dom_bytes / dom_cnt
+    achieved = dom_bytes_launch / dom_avg_s / 1e9
     iter_s = sum(prof[p][0] for p in body) / max(prof["s_update"][1], 1) / 1e3
-    kernel_names = {"spmv_pivot": "k_spmv_pivot", "spmv_t": "k_spmv_t", "true_res": "k_true_res<1>",
-                    "s_update": "k_s_update", "xr_update": "k_xr_update"}
 
     # ---- standalone kernels: zSpMV on C4, zdotc / zaxpy at 1e8 ------------------
     rng = np.random.default_rng(42)
@@ -351,11 +372,12 @@ def run_zk(args, dist: Dist):
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "ms_per_step": round(e2e_step, 3),
                 "path": "solve_bicgstab(CsrMatrix, ZVector, Preconditioner) from pinned host arrays, x.data read"},
-        "roofline": {"bound": "hbm", "kernel": kernel_names.get(dominant, dominant),
+        "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 3), "peak_kind": peak_kind,
-                     "bytes_per_launch": int(B[dominant]), "avg_launch_us": round(dom_avg_s * 1e6, 1),
-                     "traffic": traffic_from_profiles(kernel_names.get(dominant, dominant))},
+                     "bytes_per_launch": int(dom_bytes_launch), "avg_launch_us": round(dom_avg_s * 1e6, 1),
+                     "launches_per_solve": int(dom_cnt),
+                     "traffic": traffic_from_profiles(dominant, args.config)},
         "clocks": clocks,
         "gpu_launches": int(launches),
         "sub_metrics": sub,

@@ -200,8 +200,8 @@ def launch_count() -> int:
     return c.value
 
 
-PHASES = ("setup", "p_first", "pivot_first", "s_update", "x_alpha", "true_res_s", "spmv_t", "xr_update",
-          "true_res", "p_next", "spmv_pivot")
+PHASES = ("setup", "p_first", "pivot_first", "pivot_first_dot", "s_update", "x_alpha", "true_res_s", "spmv_t",
+          "tt_ts", "xr_update", "true_res", "p_next", "spmv_pivot", "pivot_dot")
 
 
 def event_record(slot: int) -> None:

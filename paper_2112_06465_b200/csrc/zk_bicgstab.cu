@@ -38,8 +38,6 @@
 namespace zk {
 
 SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv);
-bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
-             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid);
 size_t pipe_smem_bytes(const SellView& v, size_t extra);
 unsigned pipe_grid(const zk_csr* A);
 
@@ -189,52 +187,82 @@ __device__ __forceinline__ void pivot_to_alpha(SolverState* st, double2 pivot) {
     st->alpha = cdiv_py(st->rho, pivot);
 }
 
-// ---- K2: v = A p^, <r~, v> -> pivot, alpha (krylov.py:267-271) ----
+// ---- K2 / K4 SpMV: v = A p^, t = A s^ (plain pipeline, all 7 consumer warps) ----
+// The reductions that follow them (<r~, v>; <t, t> and <t, s>) run as a
+// separate pass on the level-1 engine: the vector was just written and is
+// half L2-resident, and the pass costs ~45 us at C4 against the ~150-200 us
+// a reducer warp inside the SpMV cost (profiles/r02: 858 -> 2 kernels).
+struct PhaseSpmvBody {
+    static constexpr int kNC = 0, kNR = 0, kSV = 0;
+    double2* __restrict__ y;
+    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[1], const double2 (&)[1], double2 (&)[1],
+                                        double (&)[1]) {
+        y[r] = v[0];
+    }
+    __device__ __forceinline__ void finish(const double*) {}
+};
+
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_phase(SellView A, const double2* __restrict__ x,
+                                                                double2* __restrict__ y, const SolverState* st) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (st->done) return;
+    PhaseSpmvBody body{y};
+    const RedCfg R{};
+    sell_run<1>(A, x, nullptr, body, R, smem);
+}
+
+// ---- K2 pass: <r~, v> -> pivot, alpha (krylov.py:268-271) ----
 // Last kernel of the loop body: sets the graph's WHILE condition (the
 // prologue instance, use_cond = 0, runs the first iteration's K2).
-struct PivotBody {
-    static constexpr int kNC = 1, kNR = 0, kSV = 1;  // staged: r~
-    static constexpr int kNP = 2 * kNC + kNR;
+struct PivotOp {
+    using V = double2;
+    static constexpr int NIN = 2;  // r~, v
+    bool fma;
+    __device__ __forceinline__ double2 apply(int64_t, const double2 (&v)[2]) const {
+        return f1(conjz(v[0]), v[1], fma);
+    }
+};
+
+struct PivotFin {
+    static constexpr int kNP = 2;
     SolverBufs B;
     cudaGraphConditionalHandle cond;
     int use_cond;
-    __device__ void row(int64_t row, const double2 (&av)[1], const double2 (&sv)[1], double2 (&tc)[1], double (&)[1]) {
-        B.v[row] = av[0];
-        tc[0] = f1(conjz(sv[0]), av[0], B.fma);
-    }
     __device__ void finish(const double* t) {
         SolverState* st = B.st;
-        st->counter = 0;
         pivot_to_alpha(st, make_double2(t[0], t[1]));
         if (use_cond) cudaGraphSetConditional(cond, st->done ? 0u : 1u);
     }
 };
 
-__global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_pivot(SellView A, SolverBufs B, RedCfg R,
-                                                                   cudaGraphConditionalHandle cond, int use_cond) {
+__global__ void __launch_bounds__(kL1Threads, 1) k_pivot_pass(SolverBufs B, L1View P, cudaGraphConditionalHandle cond,
+                                                              int use_cond) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (B.st->done) {
         if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
         return;
     }
-    PivotBody body{B, cond, use_cond};
-    sell_run<1>(A, B.ph, nullptr, body, R, smem);
+    PivotOp op{B.fma};
+    PivotFin fin{B, cond, use_cond};
+    l1_pipeline(P, op, fin, smem);
 }
 
-// ---- K4: t = A s^, <t,t>, <t,s> -> omega (krylov.py:281-287) ----
-struct TBody {
-    static constexpr int kNC = 2, kNR = 0, kSV = 1;  // staged: s
-    static constexpr int kNP = 2 * kNC + kNR;
-    SolverBufs B;
-    __device__ void row(int64_t row, const double2 (&at)[1], const double2 (&sv)[1], double2 (&tc)[2], double (&)[1]) {
-        B.t[row] = at[0];
-        const double2 ct = conjz(at[0]);
-        tc[0] = f1(ct, at[0], B.fma);
-        tc[1] = f1(ct, sv[0], B.fma);
+// ---- K4 pass: <t, t>, <t, s> -> omega (krylov.py:282-287) ----
+struct TOp {
+    using V = cplx2;
+    static constexpr int NIN = 2;  // t, s
+    bool fma;
+    __device__ __forceinline__ cplx2 apply(int64_t, const double2 (&v)[2]) const {
+        const double2 ct = conjz(v[0]);
+        return {f1(ct, v[0], fma), f1(ct, v[1], fma)};
     }
+};
+
+struct TFin {
+    static constexpr int kNP = 4;
+    SolverBufs B;
     __device__ void finish(const double* t) {
         SolverState* st = B.st;
-        st->counter = 0;
         const double2 tt = make_double2(t[0], t[1]), ts = make_double2(t[2], t[3]);
         if (small_py(tt)) {
             stop(st, ST_BREAKDOWN, BD_TT);
@@ -246,11 +274,12 @@ struct TBody {
     }
 };
 
-__global__ void __launch_bounds__(kRedPipeThreads, 1) k_spmv_t(SellView A, SolverBufs B, RedCfg R) {
+__global__ void __launch_bounds__(kL1Threads, 1) k_tt_ts_pass(SolverBufs B, L1View P) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (B.st->done) return;
-    TBody body{B};
-    sell_run<1>(A, B.sh, nullptr, body, R, smem);
+    TOp op{B.fma};
+    TFin fin{B};
+    l1_pipeline(P, op, fin, smem);
 }
 
 // ---- true residual ||b + F1(-1, A x)|| / ||b|| (krylov.py:183-186) ----
@@ -450,63 +479,78 @@ struct Launch {
     SolverPlan* P;
     // ring geometry + dynamic smem of the SpMV-phase kernels (their reducer
     // stashes and staged vectors differ): setup, K2, K4, K6x/K61
-    SellView As, Ap, At, Ar;
-    size_t smem_s, smem_p, smem_t, smem_r;
+    SellView As, Ar;
+    size_t smem_s, smem_r;
     RedCfg red;
     PlanPtrs pc, pr;
     unsigned nb, ew, pg;      // blocks, elementwise grid, SpMV grid
     RankCounts one;           // {nblocks}: the 1-GPU fold's partial count
-    // K3 / K5 on the TMA-fed engine (zk_l1pipe.cuh)
-    L1View l1s, l1x;
-    size_t smem_l1s = 0, smem_l1x = 0;
-    unsigned grid_l1s = 0, grid_l1x = 0;
+    // K3 / K5 and the K2 / K4 reduction passes on the TMA-fed engine (zk_l1pipe.cuh)
+    L1View l1s, l1x, l1p, l1t;
+    size_t smem_l1s = 0, smem_l1x = 0, smem_l1p = 0, smem_l1t = 0;
+    unsigned grid_l1s = 0, grid_l1x = 0, grid_l1p = 0, grid_l1t = 0;
+    SellView Apl;             // plain SpMV phases (K2, K4 products)
+    size_t smem_pl = 0;
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
 // kernel and ev[k+1] after it (prologue phases 0-2, body phases 3-10).
 struct PhaseEvents {
-    cudaEvent_t ev[12] = {};
+    cudaEvent_t ev[15] = {};
     bool on = false;
     void rec(int k, cudaStream_t s) {
         if (on) ZK_CUDA(cudaEventRecord(ev[k], s));
     }
 };
 
+// Phases (zk_profile_read order): prologue 0 setup, 1 p_first, 2 pivot_first
+// (SpMV), 3 pivot_first_dot; body 4 s_update, 5 x_alpha, 6 true_res_s,
+// 7 spmv_t, 8 tt_ts, 9 xr_update, 10 true_res, 11 p_next, 12 spmv_pivot,
+// 13 pivot_dot.  ev[k] is recorded before phase k's kernel, ev[k+1] after it.
 void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
+    SolverBufs B = L.P->bufs;
     if (pe) pe->rec(0, s);
-    k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, L.P->bufs, L.red);
+    k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red);
     if (pe) pe->rec(1, s);
-    k_p_first<<<L.ew, 256, 0, s>>>(L.P->bufs);
+    k_p_first<<<L.ew, 256, 0, s>>>(B);
     if (pe) pe->rec(2, s);
-    k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.red, 0, 0);
+    k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
     if (pe) pe->rec(3, s);
+    k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0);
+    if (pe) pe->rec(4, s);
 }
-constexpr int kPrologueKernels = 3;
+constexpr int kPrologueKernels = 4;
 
-// One iteration: K3, [K3x, K6x], K4, K5, K61, then the next iteration's Kp
-// and K2 (K61 first, so x is still in L2 when its SpMV gathers it).
+// One iteration: K3, [K3x, K6x], K4 (SpMV + pass), K5, K61, then the next
+// iteration's Kp and K2 (SpMV + pass; K61 first, so x is still in L2 when
+// its SpMV gathers it).
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
-    if (pe) pe->rec(3, s);
-    k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(L.P->bufs, L.l1s);
+    SolverBufs B = L.P->bufs;
     if (pe) pe->rec(4, s);
-    k_x_alpha<<<L.ew, 256, 0, s>>>(L.P->bufs);
+    k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s);
     if (pe) pe->rec(5, s);
-    k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
+    k_x_alpha<<<L.ew, 256, 0, s>>>(B);
     if (pe) pe->rec(6, s);
-    k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, L.P->bufs, L.red);
+    k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
     if (pe) pe->rec(7, s);
-    k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(L.P->bufs, L.l1x);
+    k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st);
     if (pe) pe->rec(8, s);
-    k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, L.P->bufs, L.red);
+    k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t);
     if (pe) pe->rec(9, s);
-    k_p_next<<<L.ew, 256, 0, s>>>(L.P->bufs);
+    k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x);
     if (pe) pe->rec(10, s);
-    k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, L.P->bufs, L.red, cond, use_cond);
+    k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
     if (pe) pe->rec(11, s);
+    k_p_next<<<L.ew, 256, 0, s>>>(B);
+    if (pe) pe->rec(12, s);
+    k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
+    if (pe) pe->rec(13, s);
+    k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
+    if (pe) pe->rec(14, s);
 }
-constexpr int kBodyKernels = 8;   // launches per loop trip
-constexpr int kBodyPhases = 8;    // timed phases per loop trip (ev[3..11])
+constexpr int kBodyKernels = 10;  // launches per loop trip
+constexpr int kBodyPhases = 10;   // timed phases per loop trip (ev[4..14])
 
 void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
     ZK_CUDA(cudaEventSynchronize(pe.ev[last + 1]));
@@ -520,8 +564,9 @@ void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
 
 void set_attrs(const Launch& L) {
     smem_attr(k_setup, L.smem_s);
-    smem_attr(k_spmv_pivot, L.smem_p);
-    smem_attr(k_spmv_t, L.smem_t);
+    smem_attr(k_spmv_phase, L.smem_pl);
+    smem_attr(k_pivot_pass, L.smem_l1p);
+    smem_attr(k_tt_ts_pass, L.smem_l1t);
     smem_attr(k_true_res<0>, L.smem_r);
     smem_attr(k_true_res<1>, L.smem_r);
     smem_attr(k_s_update_pipe, L.smem_l1s);
@@ -623,19 +668,14 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     Launch L;
     L.c = c;
     L.P = P;
-    const size_t ex_s = RedSmem<1, 2>::kBytes, ex_p = RedSmem<1, 0>::kBytes, ex_t = RedSmem<2, 0>::kBytes,
-                 ex_r = RedSmem<0, 1>::kBytes;
+    const size_t ex_s = RedSmem<1, 2>::kBytes, ex_r = RedSmem<0, 1>::kBytes;
     L.As = sell_view(A, c, ex_s, 1);
     L.As.sv[0] = B.b;
-    L.Ap = sell_view(A, c, ex_p, 1);
-    L.Ap.sv[0] = B.rs;
-    L.At = sell_view(A, c, ex_t, 1);
-    L.At.sv[0] = B.s;
     L.Ar = sell_view(A, c, ex_r, 1);
     L.Ar.sv[0] = B.b;
+    L.Apl = sell_view(A, c, 0, 0);
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
-    L.smem_p = pipe_smem_bytes(L.Ap, ex_p);
-    L.smem_t = pipe_smem_bytes(L.At, ex_t);
+    L.smem_pl = pipe_smem_bytes(L.Apl, 0);
     L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
@@ -655,8 +695,15 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
         const int8_t al3[3] = {0, 0, 0};
         const double2* in5[6] = {B.x, B.ph, B.jacobi ? B.sh : nullptr, B.s, B.t, B.rs};
         const int8_t al5[6] = {0, 0, 3, 0, 0, 0};
+        // K2 pass stages r~, v; K4 pass t, s
+        const double2* inp[2] = {B.rs, B.v};
+        const double2* int_[2] = {B.t, B.s};
+        const int8_t al2[2] = {0, 0};
         if (n > 0 && (!l1_view(c, n, kReal, in3, al3, 3, slots, partials, L.l1s, L.smem_l1s, L.grid_l1s) ||
-                      !l1_view(c, n, kComplex, in5, al5, 6, slots, partials, L.l1x, L.smem_l1x, L.grid_l1x)))
+                      !l1_view(c, n, kComplex, in5, al5, 6, slots, partials, L.l1x, L.smem_l1x, L.grid_l1x) ||
+                      !l1_view(c, n, kComplex, inp, al2, 2, slots, partials, L.l1p, L.smem_l1p, L.grid_l1p) ||
+                      !l1_view(c, n, kComplex, int_, al2, 2, slots, partials, L.l1t, L.smem_l1t, L.grid_l1t,
+                               (int)sizeof(cplx2))))
             throw ZkError{ZK_ERR_CUDA, "level-1 engine geometry"};
     }
     set_attrs(L);
@@ -846,11 +893,21 @@ void dist_phase(DistSolver* D, int phase) {
     switch (phase) {
         case ZK_DPHASE_SETUP: k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); break;
         case ZK_DPHASE_P_FIRST: k_p_first<<<L.ew, 256, 0, s>>>(B); break;
-        case ZK_DPHASE_PIVOT: k_spmv_pivot<<<L.pg, kRedPipeThreads, L.smem_p, s>>>(L.Ap, B, L.red, 0, 0); break;
+        case ZK_DPHASE_PIVOT:
+            k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
+            ZK_CUDA(cudaGetLastError());
+            D->c->launches++;
+            k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0);
+            break;
         case ZK_DPHASE_S_UPDATE: k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s); break;
         case ZK_DPHASE_X_ALPHA: k_x_alpha<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_TRUE_RES_S: k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
-        case ZK_DPHASE_SPMV_T: k_spmv_t<<<L.pg, kRedPipeThreads, L.smem_t, s>>>(L.At, B, L.red); break;
+        case ZK_DPHASE_SPMV_T:
+            k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st);
+            ZK_CUDA(cudaGetLastError());
+            D->c->launches++;
+            k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t);
+            break;
         case ZK_DPHASE_XR_UPDATE: k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); break;
         case ZK_DPHASE_TRUE_RES: k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_P_NEXT: k_p_next<<<L.ew, 256, 0, s>>>(B); break;
@@ -871,10 +928,10 @@ void dist_finish(DistSolver* D, int phase, const int64_t* rank_blocks) {
     const int64_t mb = D->maxb;
     switch (phase) {
         case ZK_DPHASE_SETUP: k_fold_finish<<<1, 32, 0, s>>>(SetupBody{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_PIVOT: k_fold_finish<<<1, 32, 0, s>>>(PivotBody{B, 0, 0}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_PIVOT: k_fold_finish<<<1, 32, 0, s>>>(PivotFin{B, 0, 0}, g, nr, mb, rc, 0); break;
         case ZK_DPHASE_S_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(SUpdFinish{B}, g, nr, mb, rc, 0); break;
         case ZK_DPHASE_TRUE_RES_S: k_fold_finish<<<1, 32, 0, s>>>(ResBody<0>{B}, g, nr, mb, rc, 1); break;
-        case ZK_DPHASE_SPMV_T: k_fold_finish<<<1, 32, 0, s>>>(TBody{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_SPMV_T: k_fold_finish<<<1, 32, 0, s>>>(TFin{B}, g, nr, mb, rc, 0); break;
         case ZK_DPHASE_XR_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(XrFinish{B}, g, nr, mb, rc, 0); break;
         case ZK_DPHASE_TRUE_RES: k_fold_finish<<<1, 32, 0, s>>>(ResBody<1>{B}, g, nr, mb, rc, 0); break;
         default: throw ZkError{ZK_ERR_PARAMETER, "phase has no reduction"};

@@ -260,7 +260,7 @@ double* fold_slots(zk_context* c, int64_t count) {
 // staged inputs; false when the plans do not fit the engine (tail block with
 // more stages than a full one), so the caller takes the block-per-CTA path.
 bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
-             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid) {
+             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid, int vbytes) {
     if (n <= 0) return false;
     const PlanPtrs p = c->plans_for(n, kBlock, kind);
     const PlanHeader* hf = reinterpret_cast<const PlanHeader*>(c->plan_host(kBlock - 1, kind));
@@ -280,7 +280,7 @@ bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, c
     }
     P.nin = staged;
     P.slot_bytes = staged * kStageMaxElems * 16;
-    const size_t head = kind == kComplex ? L1Smem<double2>::kHead : L1Smem<double>::kHead;
+    const size_t head = l1_head_bytes(vbytes ? vbytes : (kind == kComplex ? 16 : 8));
     const size_t limit = 227 * 1024 - kL1StaticSmem;
     int ns = (int)((limit - head) / (size_t)P.slot_bytes);
     if (ns > L1Smem<double>::kMaxSlots) ns = L1Smem<double>::kMaxSlots;

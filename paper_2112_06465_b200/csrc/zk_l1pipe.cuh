@@ -56,6 +56,13 @@ struct L1View {
     double* partials;             // stored partials (nblocks * NP) when slots == nullptr
 };
 
+// Engine geometry for a DEFAULT_PLAN pass over n elements (zk_blas1.cu):
+// staged inputs in[0..nin_op) (null = alias), fold slots or stored partials,
+// reduction terms of vbytes (0: 16 complex / 8 real).  False when it does
+// not fit the engine.
+bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
+             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid, int vbytes = 0);
+
 template <typename V>
 struct L1Smem {
     // [full mbarriers ns][empty mbarriers ns][blkdone 2][nodefree 2][tags ns]
@@ -69,8 +76,11 @@ struct L1Smem {
     static constexpr size_t kHead = (kBars + kTags + kNodes + kV0 + 2 * kPlanBytes + 127) / 128 * 128;
 };
 
-inline size_t l1_smem_bytes(int ns, int slot_bytes, bool complex_terms) {
-    return (complex_terms ? L1Smem<double2>::kHead : L1Smem<double>::kHead) + (size_t)ns * slot_bytes;
+// Shared-memory head (everything but the ring) for reduction terms of vbytes.
+inline size_t l1_head_bytes(int vbytes) {
+    using S = L1Smem<double>;
+    const size_t v0 = 2 * (size_t)vbytes > 16 ? 2 * (size_t)vbytes : 16;
+    return (S::kBars + S::kTags + 2 * (size_t)kL1Nodes * vbytes + v0 + 2 * S::kPlanBytes + 127) / 128 * 128;
 }
 
 // Copies a plan blob (header..stage table) into shared memory; whole warp.

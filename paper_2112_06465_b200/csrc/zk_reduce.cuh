@@ -48,6 +48,26 @@ template <> struct VT<double> {
     static __device__ __forceinline__ double shfl_down(double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); }
 };
 
+// Two complex reductions summed side by side in the same (complex) order,
+// e.g. <t, t> and <t, s> of BiCGStab's omega (krylov.py:282-286).
+struct cplx2 {
+    double2 a, b;
+};
+template <> struct VT<cplx2> {
+    static constexpr int lanes = 4;
+    static __device__ __forceinline__ cplx2 add(cplx2 x, cplx2 y) { return {cadd(x.a, y.a), cadd(x.b, y.b)}; }
+    static __device__ __forceinline__ cplx2 negzero() {
+        return {make_double2(-0.0, -0.0), make_double2(-0.0, -0.0)};
+    }
+    static __device__ __forceinline__ cplx2 zero() { return {make_double2(0.0, 0.0), make_double2(0.0, 0.0)}; }
+    static __device__ __forceinline__ cplx2 shfl(cplx2 v, int src) {
+        return {VT<double2>::shfl(v.a, src), VT<double2>::shfl(v.b, src)};
+    }
+    static __device__ __forceinline__ cplx2 shfl_down(cplx2 v, int d) {
+        return {VT<double2>::shfl_down(v.a, d), VT<double2>::shfl_down(v.b, d)};
+    }
+};
+
 struct PlanPtrs {
     const char* full;  // plan for full blocks (L = block_size - 1)
     const char* tail;  // plan for the last, partial block (may equal full)
