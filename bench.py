@@ -188,6 +188,8 @@ def algorithmic_bytes(n: int, nnz: int):
     return {
         "spmv": A,
         "spmv_pivot": A,                      # v = A p^ (plain pipeline)
+        "spmv2": A + 32 * n,                  # A x and v = A p^ in one matrix pass (two gathers, two writes)
+        "res_pass": 32 * n,                   # ||b - A x||: b, A x
         "pivot_first": A,
         "pivot_dot": 32 * n,                  # <r~, v>: r~, v
         "pivot_first_dot": 32 * n,
@@ -301,9 +303,10 @@ def run_zk(args, dist: Dist):
                 entry["gbs"] = round(B[name] / (avg * 1e-3) / 1e9, 1)
             phases[name] = entry
     body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "tt_ts", "xr_update", "true_res", "p_next",
-                        "spmv_pivot", "pivot_dot")
+                        "spmv2", "spmv_pivot", "res_pass", "pivot_dot")
             if p in phases]
-    kernel_names = {"spmv_pivot": "k_spmv_phase", "spmv_t": "k_spmv_phase", "true_res": "k_true_res<1>",
+    kernel_names = {"spmv2": "k_spmv2_phase", "spmv_t": "k_spmv_phase", "spmv_pivot": "k_spmv_phase",
+                    "res_pass": "k_res_pass", "true_res": "k_true_res<1>",
                     "s_update": "k_s_update_pipe", "xr_update": "k_xr_update_pipe", "tt_ts": "k_tt_ts_pass",
                     "pivot_dot": "k_pivot_pass", "p_next": "k_p_next"}
     # dominant kernel = the most device time per solve, summed over the

@@ -332,6 +332,53 @@ __global__ void __launch_bounds__(kRedPipeThreads, 1) k_true_res(SellView A, Sol
     sell_run<1>(A, B.x, nullptr, body, R, smem);
 }
 
+// ---- K61 + next K2 in ONE matrix pass: t = A x and v = A p^ ------------------
+// (krylov.py:291 true residual, :267 next pivot product).  Kp runs first, so
+// both gathered vectors are final; the residual's reduction pass then runs
+// before the pivot's, keeping the reference's order of checks (record/stop,
+// then the next pivot).  t is free here (K5 consumed it; the next K4
+// rewrites it).  One stream of the 4.3 GB matrix serves both products.
+struct PhaseSpmv2Body {
+    static constexpr int kNC = 0, kNR = 0, kSV = 0;
+    double2* __restrict__ y0;
+    double2* __restrict__ y1;
+    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[2], const double2 (&)[1], double2 (&)[1],
+                                        double (&)[1]) {
+        y0[r] = v[0];
+        y1[r] = v[1];
+    }
+    __device__ __forceinline__ void finish(const double*) {}
+};
+
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv2_phase(SellView A, const double2* __restrict__ x0,
+                                                                 const double2* __restrict__ x1,
+                                                                 double2* __restrict__ y0, double2* __restrict__ y1,
+                                                                 const SolverState* st) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (st->done) return;
+    PhaseSpmv2Body body{y0, y1};
+    const RedCfg R{};
+    sell_run<2>(A, x0, x1, body, R, smem);
+}
+
+// true residual pass: ||b + F1(-1, A x)||^2 over (b, A x) -> record / stop
+struct ResOp {
+    using V = double;
+    static constexpr int NIN = 2;  // b, A x
+    bool fma;
+    __device__ __forceinline__ double apply(int64_t, const double2 (&v)[2]) const {
+        return abs2_np(cadd(v[0], f1(make_double2(-1.0, 0.0), v[1], fma)));
+    }
+};
+
+__global__ void __launch_bounds__(kL1Threads, 1) k_res_pass(SolverBufs B, L1View P) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (B.st->done) return;
+    ResOp op{B.fma};
+    ResBody<1> fin{B};
+    l1_pipeline(P, op, fin, smem);
+}
+
 __global__ void k_fill_empty(double* p, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = __longlong_as_double((long long)kSlotEmpty);
@@ -489,82 +536,111 @@ struct Launch {
     L1View l1s, l1x, l1p, l1t;
     size_t smem_l1s = 0, smem_l1x = 0, smem_l1p = 0, smem_l1t = 0;
     unsigned grid_l1s = 0, grid_l1x = 0, grid_l1p = 0, grid_l1t = 0;
-    SellView Apl;             // plain SpMV phases (K2, K4 products)
-    size_t smem_pl = 0;
+    SellView Apl, Apl2;       // plain SpMV phases (K4, first K2; K61 + K2 with two vectors)
+    size_t smem_pl = 0, smem_pl2 = 0;
+    bool fuse2 = false;       // one matrix pass for K61 + K2 (needs x staging: consumer-bound otherwise)
+    L1View l1r;               // true-residual pass
+    size_t smem_l1r = 0;
+    unsigned grid_l1r = 0;
 };
 
 // Phase events for zk_profile_enable: ev[k] is recorded before phase k's
 // kernel and ev[k+1] after it (prologue phases 0-2, body phases 3-10).
+// Solver phases, in zk_profile_read order (include/zk.h ZK_NPHASES):
+enum Phase : int {
+    PH_SETUP, PH_P_FIRST, PH_PIVOT_FIRST, PH_PIVOT_FIRST_DOT,          // prologue
+    PH_S_UPDATE, PH_X_ALPHA, PH_TRUE_RES_S, PH_SPMV_T, PH_TT_TS, PH_XR_UPDATE,
+    PH_TRUE_RES, PH_P_NEXT, PH_SPMV_PIVOT, PH_SPMV2, PH_RES_PASS, PH_PIVOT_DOT,
+    PH_COUNT
+};
+
+// Events bracketing each phase's kernel (host-driven profiling loop only).
 struct PhaseEvents {
-    cudaEvent_t ev[15] = {};
+    cudaEvent_t beg[PH_COUNT] = {}, end[PH_COUNT] = {};
+    bool used[PH_COUNT] = {};
     bool on = false;
-    void rec(int k, cudaStream_t s) {
-        if (on) ZK_CUDA(cudaEventRecord(ev[k], s));
+    cudaStream_t s = nullptr;
+    void b(int k) {
+        if (on) {
+            ZK_CUDA(cudaEventRecord(beg[k], s));
+            used[k] = true;
+        }
+    }
+    void e(int k) {
+        if (on) ZK_CUDA(cudaEventRecord(end[k], s));
     }
 };
 
-// Phases (zk_profile_read order): prologue 0 setup, 1 p_first, 2 pivot_first
-// (SpMV), 3 pivot_first_dot; body 4 s_update, 5 x_alpha, 6 true_res_s,
-// 7 spmv_t, 8 tt_ts, 9 xr_update, 10 true_res, 11 p_next, 12 spmv_pivot,
-// 13 pivot_dot.  ev[k] is recorded before phase k's kernel, ev[k+1] after it.
+// Wraps one kernel launch in its phase's events (a no-op without profiling).
+struct PhaseScope {
+    PhaseEvents* pe;
+    int k;
+    PhaseScope(PhaseEvents* p, int kk) : pe(p), k(kk) {
+        if (pe) pe->b(k);
+    }
+    ~PhaseScope() {
+        if (pe) pe->e(k);
+    }
+};
+
 void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
     SolverBufs B = L.P->bufs;
-    if (pe) pe->rec(0, s);
-    k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red);
-    if (pe) pe->rec(1, s);
-    k_p_first<<<L.ew, 256, 0, s>>>(B);
-    if (pe) pe->rec(2, s);
-    k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
-    if (pe) pe->rec(3, s);
-    k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0);
-    if (pe) pe->rec(4, s);
+    { PhaseScope ps(pe, PH_SETUP); k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); }
+    { PhaseScope ps(pe, PH_P_FIRST); k_p_first<<<L.ew, 256, 0, s>>>(B); }
+    { PhaseScope ps(pe, PH_PIVOT_FIRST); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
+    { PhaseScope ps(pe, PH_PIVOT_FIRST_DOT); k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0); }
 }
 constexpr int kPrologueKernels = 4;
 
-// One iteration: K3, [K3x, K6x], K4 (SpMV + pass), K5, K61, then the next
-// iteration's Kp and K2 (SpMV + pass; K61 first, so x is still in L2 when
-// its SpMV gathers it).
+// One iteration: K3, [K3x, K6x], K4 (SpMV + pass), K5; then either K61
+// (residual reduction fused into its SpMV), Kp, the next K2's SpMV -- or,
+// with L.fuse2, Kp and ONE matrix pass for K61's A x and the next K2's A p^
+// followed by the residual pass (record / stop); and the pivot pass.
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
     SolverBufs B = L.P->bufs;
-    if (pe) pe->rec(4, s);
-    k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s);
-    if (pe) pe->rec(5, s);
-    k_x_alpha<<<L.ew, 256, 0, s>>>(B);
-    if (pe) pe->rec(6, s);
-    k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
-    if (pe) pe->rec(7, s);
-    k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st);
-    if (pe) pe->rec(8, s);
-    k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t);
-    if (pe) pe->rec(9, s);
-    k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x);
-    if (pe) pe->rec(10, s);
-    k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
-    if (pe) pe->rec(11, s);
-    k_p_next<<<L.ew, 256, 0, s>>>(B);
-    if (pe) pe->rec(12, s);
-    k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
-    if (pe) pe->rec(13, s);
-    k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
-    if (pe) pe->rec(14, s);
+    { PhaseScope ps(pe, PH_S_UPDATE); k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s); }
+    { PhaseScope ps(pe, PH_X_ALPHA); k_x_alpha<<<L.ew, 256, 0, s>>>(B); }
+    { PhaseScope ps(pe, PH_TRUE_RES_S); k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); }
+    { PhaseScope ps(pe, PH_SPMV_T); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st); }
+    { PhaseScope ps(pe, PH_TT_TS); k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t); }
+    { PhaseScope ps(pe, PH_XR_UPDATE); k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); }
+    if (L.fuse2) {
+        { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
+        {
+            PhaseScope ps(pe, PH_SPMV2);
+            k_spmv2_phase<<<L.pg, kPipeThreads, L.smem_pl2, s>>>(L.Apl2, B.x, B.ph, B.t, B.v, B.st);
+        }
+        { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
+    } else {
+        { PhaseScope ps(pe, PH_TRUE_RES); k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); }
+        { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
+        { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
+    }
+    {
+        PhaseScope ps(pe, PH_PIVOT_DOT);
+        k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
+    }
 }
-constexpr int kBodyKernels = 10;  // launches per loop trip
-constexpr int kBodyPhases = 10;   // timed phases per loop trip (ev[4..14])
+constexpr int kBodyKernels = 10;  // launches per loop trip (either shape)
 
-void accumulate(zk_context* c, PhaseEvents& pe, int first, int last) {
-    ZK_CUDA(cudaEventSynchronize(pe.ev[last + 1]));
-    for (int k = first; k <= last; ++k) {
+void accumulate(zk_context* c, PhaseEvents& pe) {
+    for (int k = 0; k < PH_COUNT; ++k) {
+        if (!pe.used[k]) continue;
+        ZK_CUDA(cudaEventSynchronize(pe.end[k]));
         float ms = 0.f;
-        ZK_CUDA(cudaEventElapsedTime(&ms, pe.ev[k], pe.ev[k + 1]));
+        ZK_CUDA(cudaEventElapsedTime(&ms, pe.beg[k], pe.end[k]));
         c->prof_ms[k] += ms;
         c->prof_n[k] += 1;
+        pe.used[k] = false;
     }
 }
 
 void set_attrs(const Launch& L) {
     smem_attr(k_setup, L.smem_s);
     smem_attr(k_spmv_phase, L.smem_pl);
+    smem_attr(k_spmv2_phase, L.smem_pl2);
+    smem_attr(k_res_pass, L.smem_l1r);
     smem_attr(k_pivot_pass, L.smem_l1p);
     smem_attr(k_tt_ts_pass, L.smem_l1t);
     smem_attr(k_true_res<0>, L.smem_r);
@@ -674,8 +750,10 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.Ar = sell_view(A, c, ex_r, 1);
     L.Ar.sv[0] = B.b;
     L.Apl = sell_view(A, c, 0, 0);
+    L.Apl2 = sell_view(A, c, 0, 0);
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_pl = pipe_smem_bytes(L.Apl, 0);
+    L.smem_pl2 = pipe_smem_bytes(L.Apl2, 0);
     L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
@@ -698,12 +776,14 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
         // K2 pass stages r~, v; K4 pass t, s
         const double2* inp[2] = {B.rs, B.v};
         const double2* int_[2] = {B.t, B.s};
+        const double2* inr[2] = {B.b, B.t};  // residual pass: b, A x (in t)
         const int8_t al2[2] = {0, 0};
         if (n > 0 && (!l1_view(c, n, kReal, in3, al3, 3, slots, partials, L.l1s, L.smem_l1s, L.grid_l1s) ||
                       !l1_view(c, n, kComplex, in5, al5, 6, slots, partials, L.l1x, L.smem_l1x, L.grid_l1x) ||
                       !l1_view(c, n, kComplex, inp, al2, 2, slots, partials, L.l1p, L.smem_l1p, L.grid_l1p) ||
                       !l1_view(c, n, kComplex, int_, al2, 2, slots, partials, L.l1t, L.smem_l1t, L.grid_l1t,
-                               (int)sizeof(cplx2))))
+                               (int)sizeof(cplx2)) ||
+                      !l1_view(c, n, kReal, inr, al2, 2, slots, partials, L.l1r, L.smem_l1r, L.grid_l1r)))
             throw ZkError{ZK_ERR_CUDA, "level-1 engine geometry"};
     }
     set_attrs(L);
@@ -754,21 +834,28 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     } else {  // host-driven loop (ZK_SOLVER_LOOP=host, or phase profiling)
         PhaseEvents pe;
         pe.on = c->profile;
+        pe.s = s;
         if (pe.on)
-            for (auto& e : pe.ev) ZK_CUDA(cudaEventCreate(&e));
+            for (int k = 0; k < PH_COUNT; ++k) {
+                ZK_CUDA(cudaEventCreate(&pe.beg[k]));
+                ZK_CUDA(cudaEventCreate(&pe.end[k]));
+            }
         launch_prologue(L, s, &pe);
         ZK_CUDA(cudaGetLastError());
-        if (pe.on) accumulate(c, pe, 0, kPrologueKernels - 1);
+        if (pe.on) accumulate(c, pe);
         for (;;) {
             launch_body(L, s, 0, 0, &pe);
             ZK_CUDA(cudaGetLastError());
             ZK_CUDA(cudaMemcpyAsync(&out, B.st, sizeof(out), cudaMemcpyDeviceToHost, s));
             ZK_CUDA(cudaStreamSynchronize(s));
-            if (pe.on) accumulate(c, pe, kPrologueKernels, kPrologueKernels + kBodyPhases - 1);
+            if (pe.on) accumulate(c, pe);
             if (out.done) break;
         }
         if (pe.on)
-            for (auto& e : pe.ev) cudaEventDestroy(e);
+            for (int k = 0; k < PH_COUNT; ++k) {
+                cudaEventDestroy(pe.beg[k]);
+                cudaEventDestroy(pe.end[k]);
+            }
     }
     c->launches += kPrologueKernels + kBodyKernels * out.trips;
     const int64_t it = out.iterations;
