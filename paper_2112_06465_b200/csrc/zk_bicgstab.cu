@@ -751,6 +751,13 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.Ar.sv[0] = B.b;
     L.Apl = sell_view(A, c, 0, 0);
     L.Apl2 = sell_view(A, c, 0, 0);
+    {
+        // one matrix pass for K61 + K2 measured slower on C4 (1703 us vs 799 +
+        // 716 us: two gathered vectors make the consumers the bottleneck);
+        // ZK_FUSE2=1 selects it for experiments
+        const char* e = std::getenv("ZK_FUSE2");
+        L.fuse2 = e && e[0] == '1';
+    }
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_pl = pipe_smem_bytes(L.Apl, 0);
     L.smem_pl2 = pipe_smem_bytes(L.Apl2, 0);
