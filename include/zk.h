@@ -151,6 +151,12 @@ zk_status zk_spmv(zk_context* ctx, const zk_csr* A, const double* x, double* y);
 zk_status zk_spmv_dotc(zk_context* ctx, const zk_csr* A, const double* x, double* y, const double* w,
                        int conjugate, double* result_host);
 
+/* Jacobi preconditioner on the device: minv[i] = 1 / A[i][i] for
+ * i < min(n_rows, n_cols), numpy's complex division bit for bit.  A missing
+ * or zero diagonal entry returns ZK_ERR_SINGULAR with *zero_row = the first
+ * such row (else -1).          replaces krylov.build_jacobi (krylov.py:106-120) */
+zk_status zk_jacobi_build(zk_context* ctx, const zk_csr* A, double* minv, int64_t* zero_row);
+
 /* ---- BiCGStab (krylov.py) ----------------------------------------------- */
 typedef struct {
     int64_t iterations;          /* SolveReport.iterations */

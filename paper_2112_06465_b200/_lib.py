@@ -96,6 +96,7 @@ SIGNATURES = {
     "zk_csr_destroy": [_vp],
     "zk_csr_bytes": [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
     "zk_spmv": [_vp, _vp, _vp, _vp],
+    "zk_jacobi_build": [_vp, _vp, _vp, ctypes.POINTER(_i64)],
     "zk_spmv_dotc": [_vp, _vp, _vp, _vp, _vp, _i, ctypes.POINTER(_d)],
     "zk_bicgstab": [_vp, _vp, _vp, _vp, _vp, _d, _i64, _vp, ctypes.POINTER(_d), ctypes.POINTER(SolveReportC)],
     "zk_bicgstab_l": [_vp, _vp, _vp, _vp, _vp, _d, _i64, _i, _vp, ctypes.POINTER(_d), ctypes.POINTER(SolveReportC),

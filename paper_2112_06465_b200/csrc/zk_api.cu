@@ -122,6 +122,7 @@ int krylov_device(zk_context* c, zk_csr* A, int solver, int ell, const double2* 
                   const double2* x0, double tol, int64_t maxit, double2* x_out, double* history_host,
                   zk_solve_report* rep, int32_t* what_j);
 void destroy_sell(zk_csr* A);
+int64_t jacobi_build_device(zk_context* c, const zk_csr* A, double2* minv);
 
 }  // namespace zk
 
@@ -661,6 +662,21 @@ zk_status zk_spmv_dotc(zk_context* c, const zk_csr* A, const double* x, double* 
         ZK_CUDA(cudaStreamSynchronize(c->stream));
         result_host[0] = c->h_result[0];
         result_host[1] = c->h_result[1];
+    });
+}
+
+zk_status zk_jacobi_build(zk_context* c, const zk_csr* A, double* minv, int64_t* zero_row) {
+    return guarded([&] {
+        need_ctx(c);
+        need(A != nullptr, ZK_ERR_PARAMETER, "null matrix");
+        need(zero_row != nullptr, ZK_ERR_PARAMETER, "null zero_row");
+        const int64_t n = A->n_rows < A->n_cols ? A->n_rows : A->n_cols;
+        need_ptr(minv, n, "minv");
+        const int64_t z = jacobi_build_device(c, A, D2(minv));
+        *zero_row = z;
+        if (z >= 0)
+            throw ZkError{ZK_ERR_SINGULAR, "zero diagonal entry at row " + std::to_string(z) +
+                                               "; Jacobi preconditioner is singular"};
     });
 }
 

@@ -538,7 +538,8 @@ struct Launch {
     unsigned grid_l1s = 0, grid_l1x = 0, grid_l1p = 0, grid_l1t = 0;
     SellView Apl, Apl2;       // plain SpMV phases (K4, first K2; K61 + K2 with two vectors)
     size_t smem_pl = 0, smem_pl2 = 0;
-    bool fuse2 = false;       // one matrix pass for K61 + K2 (needs x staging: consumer-bound otherwise)
+    bool fuse2 = false;       // one matrix pass for K61 + K2 (consumer-bound: experiments only)
+    bool respass = false;     // K61 as plain SpMV + residual pass instead of the reducer-warp SpMV
     L1View l1r;               // true-residual pass
     size_t smem_l1r = 0;
     unsigned grid_l1r = 0;
@@ -613,7 +614,13 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
         }
         { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
     } else {
-        { PhaseScope ps(pe, PH_TRUE_RES); k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); }
+        if (L.respass) {  // K61 as a plain SpMV into t + the residual pass
+            { PhaseScope ps(pe, PH_TRUE_RES); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st); }
+            { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
+        } else {
+            PhaseScope ps(pe, PH_TRUE_RES);
+            k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
+        }
         { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
         { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
     }
@@ -622,7 +629,8 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
         k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
     }
 }
-constexpr int kBodyKernels = 10;  // launches per loop trip (either shape)
+// launches per loop trip
+inline int body_kernels(const Launch& L) { return (!L.fuse2 && L.respass) ? 11 : 10; }
 
 void accumulate(zk_context* c, PhaseEvents& pe) {
     for (int k = 0; k < PH_COUNT; ++k) {
@@ -757,6 +765,9 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
         // ZK_FUSE2=1 selects it for experiments
         const char* e = std::getenv("ZK_FUSE2");
         L.fuse2 = e && e[0] == '1';
+        // K61 as plain SpMV + residual pass: 786 vs 794 us on C4 (profiles/r02)
+        const char* r = std::getenv("ZK_RESPASS");
+        L.respass = !(r && r[0] == '0');
     }
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_pl = pipe_smem_bytes(L.Apl, 0);
@@ -864,7 +875,7 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
                 cudaEventDestroy(pe.end[k]);
             }
     }
-    c->launches += kPrologueKernels + kBodyKernels * out.trips;
+    c->launches += kPrologueKernels + body_kernels(L) * out.trips;
     const int64_t it = out.iterations;
     ZK_CUDA(cudaMemcpyAsync(history_host, B.hist, sizeof(double) * (it + 1), cudaMemcpyDeviceToHost, s));
     if (out.trivial_zero) ZK_CUDA(cudaMemsetAsync(x_out, 0, vb, s));
@@ -875,7 +886,7 @@ int bicgstab_device(zk_context* c, zk_csr* A, const double2* b, const double2* m
     rep->breakdown = out.status == ST_BREAKDOWN ? out.what : 0;
     rep->final_relative_residual = history_host[it];
     rep->history_len = it + 1;
-    rep->kernel_launches = kPrologueKernels + kBodyKernels * out.trips;
+    rep->kernel_launches = kPrologueKernels + body_kernels(L) * out.trips;
     return out.status == ST_BREAKDOWN ? ZK_ERR_BREAKDOWN : ZK_OK;
 }
 

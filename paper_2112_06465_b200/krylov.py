@@ -109,14 +109,20 @@ class Preconditioner:
 
 
 def build_jacobi(A: CsrMatrix) -> Preconditioner:
-    """Inverse main diagonal (krylov.py:106-120).  Host setup: the quotient is
-    numpy's own complex division, exactly as the reference forms it."""
-    diag = A.diagonal()
-    zero = np.flatnonzero(diag == 0)
-    if zero.size:
-        raise SingularPreconditionerError(
-            f"zero diagonal entry at row {int(zero[0])}; Jacobi preconditioner is singular")
-    return Preconditioner("jacobi", np.divide(1.0, diag))
+    """Inverse main diagonal (krylov.py:106-120), built on the device
+    (zk_jacobi_build): the stored diagonal of each row, a check for missing or
+    zero entries, and numpy's complex division 1 / d bit for bit.  The
+    preconditioner's vector stays on the device until ``data`` is read."""
+    n = min(A.n_rows, A.n_cols)
+    minv = ZVector._device_new(n)
+    if n:
+        zero = ctypes.c_int64(-1)
+        status = _lib.lib().zk_jacobi_build(_lib.context(), A._device(), minv._dptr_out(), ctypes.byref(zero))
+        if status == _lib.ZK_ERR_SINGULAR:
+            raise SingularPreconditionerError(
+                f"zero diagonal entry at row {int(zero.value)}; Jacobi preconditioner is singular")
+        _lib.check(status)
+    return Preconditioner("jacobi", minv._written())
 
 
 @dataclass

@@ -171,12 +171,15 @@ class _Handle:
 def coo_to_csr(m: CooMatrix) -> CsrMatrix:
     """Sort by (row, col) and sum duplicates (host ingestion, sparse.py:174-214)."""
     n_rows, n_cols = m.n_rows, m.n_cols
-    if not m.entries:
+    if hasattr(m, "arrays"):  # array-backed (matio.ArrayCooMatrix): no tuple list
+        rows, cols, vals = m.arrays()
+    else:
+        rows = np.fromiter((e[0] for e in m.entries), dtype=np.int64, count=len(m.entries))
+        cols = np.fromiter((e[1] for e in m.entries), dtype=np.int64, count=len(m.entries))
+        vals = np.fromiter((complex(e[2]) for e in m.entries), dtype=np.complex128, count=len(m.entries))
+    if rows.shape[0] == 0:
         return CsrMatrix(n_rows, n_cols, np.zeros(0, np.complex128), np.zeros(0, np.int64),
                          np.zeros(n_rows + 1, np.int64))
-    rows = np.fromiter((e[0] for e in m.entries), dtype=np.int64, count=len(m.entries))
-    cols = np.fromiter((e[1] for e in m.entries), dtype=np.int64, count=len(m.entries))
-    vals = np.fromiter((complex(e[2]) for e in m.entries), dtype=np.complex128, count=len(m.entries))
     bad = (rows < 0) | (rows >= n_rows) | (cols < 0) | (cols >= n_cols)
     if bad.any():
         k = int(np.flatnonzero(bad)[0])
@@ -220,3 +223,11 @@ def spmv(A: CsrMatrix, x: ZVector) -> ZVector:
     xp = x._dptr()
     _lib.check(_lib.lib().zk_spmv(_lib.context(), A._device(), xp, y._dptr_out()))
     return y._written()
+
+
+def __getattr__(name):  # the reference exports its I/O from sparse (sparse.py:160-402)
+    if name in ("MatrixStats", "stats", "read_matrix_market", "write_matrix_market", "read_csr_binary",
+                "write_csr_binary"):
+        from . import matio
+        return getattr(matio, name)
+    raise AttributeError(name)

@@ -356,3 +356,48 @@ def test_acceptance_4_5_9():
     second = _criterion_4()
     for (_, _, xa, ra), (_, _, xb, rb) in zip(first, second):
         assert ra.residual_history == rb.residual_history and bits(xa.data) == bits(xb.data)
+
+
+def test_build_jacobi_device_errors_and_values():  # krylov.py:106-120, test_krylov.py:240-250
+    A = Z.CsrMatrix(2, 2, [1.0, 1.0], [0, 0], [0, 1, 2])
+    with pytest.raises(Z.SingularPreconditionerError, match="row 1"):
+        Z.build_jacobi(A)
+    M = Z.build_jacobi(Z.CsrMatrix(2, 2, [2.0, 1j], [0, 1], [0, 1, 2]))
+    assert M.data[0] == 0.5 and M.data[1] == -1j
+    with pytest.raises(Z.SingularPreconditionerError, match="row 0"):  # explicit zero on the diagonal
+        Z.build_jacobi(Z.CsrMatrix(2, 2, [0j, 1.0], [0, 1], [0, 1, 2]))
+
+
+def test_build_jacobi_device_is_numpy_division_bitwise():
+    """1 / d on the device == np.divide(1.0, d) (numpy's Smith variant), over
+    magnitudes 1e-26..1e26, pure real / pure imaginary entries and signed
+    zeros in the other part; rectangular shapes use min(n_rows, n_cols)."""
+    rng = np.random.default_rng(7)
+    n = 50000
+    d = rng.standard_normal(n) * np.exp(rng.uniform(-60, 60, n)) + 1j * (
+        rng.standard_normal(n) * np.exp(rng.uniform(-60, 60, n)))
+    d[:500] = d[:500].real + 0j
+    d[500:1000] = 1j * d[500:1000].imag
+    d[1000:1500] = d[1000:1500].real - 0j
+    A = Z.CsrMatrix(n, n, d, np.arange(n), np.arange(n + 1))
+    assert bits(Z.build_jacobi(A).data) == bits(np.divide(1.0, d))
+    # a dense-ish matrix with the diagonal among other entries, 3 x 5
+    dense = rng.standard_normal((3, 5)) + 1j * rng.standard_normal((3, 5))
+    from helpers import dense_to_csr
+    A = dense_to_csr(dense)
+    assert bits(Z.build_jacobi(A).data) == bits(np.divide(1.0, np.diag(dense)))
+
+
+def test_build_jacobi_long_rows():
+    """Diagonal entries inside rows longer than 65 (side CSR)."""
+    n = 300
+    rows, cols = [], []
+    for i in range(n):
+        cs = sorted(set([i] + list(range(0, n, 3)))) if i % 7 == 0 else [i]
+        rows += [i] * len(cs)
+        cols += cs
+    rng = np.random.default_rng(3)
+    vals = rng.standard_normal(len(cols)) + 1j * rng.standard_normal(len(cols))
+    ia = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=n))])
+    A = Z.CsrMatrix(n, n, vals, np.array(cols), ia)
+    assert bits(Z.build_jacobi(A).data) == bits(np.divide(1.0, A.diagonal()))

@@ -84,14 +84,6 @@ def test_csr_validation():  # sparse.py:79-103 / test_sparse.py:96-108
     Z.CsrMatrix(4, 4, [1.0, 2.0, 3.0], [0, 3, 1], [0, 2, 2, 2, 3])
 
 
-def test_build_jacobi_host_setup():
-    A = Z.CsrMatrix(2, 2, [1.0, 1.0], [0, 0], [0, 1, 2])
-    with pytest.raises(Z.SingularPreconditionerError, match="row 1"):
-        Z.build_jacobi(A)
-    M = Z.build_jacobi(Z.CsrMatrix(2, 2, [2.0, 1j], [0, 1], [0, 1, 2]))
-    assert M.data[0] == 0.5 and M.data[1] == -1j
-
-
 def test_diagonal_vectorised_matches_loop():
     rng = np.random.default_rng(3)
     d = (rng.random((30, 30)) < 0.2) * (rng.standard_normal((30, 30)) + 1j)
