@@ -638,6 +638,19 @@ def run_reference(args, dist: Dist):
     print(json.dumps(out), flush=True)
 
 
+def _launch_ranks(args) -> int:
+    """``--gpus N`` without a torchrun environment: start N ranks on this
+    node (torch.distributed.run, 127.0.0.1 rendezvous), one per GPU, and
+    return their exit status; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -650,7 +663,11 @@ def main():
     ap.add_argument("--no-solvers", action="store_true", help="skip the BiCGSTAB(8) / TFQMR lines")
     ap.add_argument("--config", choices=sorted(WORKLOADS), default=CONFIG, help="BASELINE system (default C4)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(_launch_ranks(args))
     dist = Dist() if args.impl == "zk" else _NoDist()
+    if args.impl == "zk" and dist.world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={dist.world}")
     try:
         if args.impl == "reference":
             run_reference(args, dist)

@@ -215,9 +215,12 @@ zk_status zk_tfqmr(zk_context* ctx, const zk_csr* A, const double* b, const doub
  *   - before SETUP / TRUE_RES_S / TRUE_RES the halo of ZK_DVEC_X, before
  *     PIVOT that of ZK_DVEC_PHAT, before SPMV_T that of ZK_DVEC_SHAT must be
  *     current (zk_dshard_pack gathers the entries a peer needs);
- *   - after every phase with a reduction, each rank's ZK_DVEC_PARTIALS
- *     (max_blocks * 4 doubles) is all-gathered into ZK_DVEC_GATHERED (rank r
- *     at r * max_blocks * 4) and zk_dshard_finish folds it.
+ *   - after a phase with a reduction, each rank's ZK_DVEC_PARTIALS is
+ *     all-gathered into ZK_DVEC_GATHERED (rank r at r * len(PARTIALS)) and
+ *     zk_dshard_finish folds it.  PARTIALS holds two slots of
+ *     4 * max_blocks doubles: SPMV_T and TRUE_RES write slot 1, every other
+ *     phase slot 0, so TRUE_RES_S + SPMV_T and XR_UPDATE + TRUE_RES can
+ *     share one all-gather (finish them in that order).
  * Phases whose work depends on the s-check (X_ALPHA, TRUE_RES_S) are no-ops
  * on the device when it did not fire, so every rank issues the same calls. */
 typedef struct zk_dshard zk_dshard;

@@ -62,6 +62,7 @@ struct SolverBufs {
     int64_t n, nblocks;
     bool jacobi, fma;
     int dist;          // row-sharded solve: block partials are folded across ranks (k_fold_finish)
+    int64_t pslot;     // row-sharded: doubles per partials slot (4 x max blocks of any rank); slot 1 at +pslot
 };
 
 
@@ -494,7 +495,7 @@ struct RankCounts {
 
 template <class Fin>
 __global__ void __launch_bounds__(32) k_fold_finish(Fin fin, const double* __restrict__ gathered, int nranks,
-                                                    int64_t maxb, RankCounts counts, int phase_gate) {
+                                                    int64_t rank_stride, RankCounts counts, int phase_gate) {
     __shared__ double scratch[2 * kFoldStage];
     const SolverState* st = fin.B.st;
     if (st->done || (phase_gate == 1 && !st->scheck)) return;
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(32) k_fold_finish(Fin fin, const double* __res
     bool first = true;
     for (int r = 0; r < nranks; ++r) {
         if (counts.n[r] <= 0) continue;
-        warp_fold_cont(gathered + (int64_t)r * maxb * NP, NP, counts.n[r], scratch, tot, first);
+        warp_fold_cont(gathered + (int64_t)r * rank_stride, NP, counts.n[r], scratch, tot, first);
         first = false;
     }
     double t[NP];
@@ -528,7 +529,7 @@ struct Launch {
     // stashes and staged vectors differ): setup, K2, K4, K6x/K61
     SellView As, Ar;
     size_t smem_s, smem_r;
-    RedCfg red;
+    RedCfg red, red1;          // reducer-warp SpMV kernels: partials slot 0 / slot 1 (row-sharded)
     PlanPtrs pc, pr;
     unsigned nb, ew, pg;      // blocks, elementwise grid, SpMV grid
     RankCounts one;           // {nblocks}: the 1-GPU fold's partial count
@@ -776,6 +777,7 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
     L.red = RedCfg{L.pc, L.pr, B.partials, &B.st->counter, B.dist, B.dist ? nullptr : B.slots};
+    L.red1 = RedCfg{L.pc, L.pr, B.partials + B.pslot, &B.st->counter, B.dist, B.dist ? nullptr : B.slots};
     L.nb = (unsigned)B.nblocks;
     L.one = RankCounts{};
     L.one.n[0] = B.nblocks;
@@ -785,7 +787,11 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
     {
         double* slots = B.dist ? nullptr : B.slots;
+        // row-sharded: two partials slots, so two reductions can share one
+        // all-gather (K6x + K4, K5 + K61; dist.py) -- slot 0: K3, K5, K2;
+        // slot 1: K4's and K61's passes
         double* partials = B.dist ? B.partials : nullptr;
+        double* partials1 = B.dist ? B.partials + B.pslot : nullptr;
         // K3 stages r, v (and minv); K5 x, p^, s^ (identity: s^ is s), s, t, r~
         const double2* in3[3] = {B.r, B.v, B.jacobi ? B.minv : nullptr};
         const int8_t al3[3] = {0, 0, 0};
@@ -799,9 +805,9 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
         if (n > 0 && (!l1_view(c, n, kReal, in3, al3, 3, slots, partials, L.l1s, L.smem_l1s, L.grid_l1s) ||
                       !l1_view(c, n, kComplex, in5, al5, 6, slots, partials, L.l1x, L.smem_l1x, L.grid_l1x) ||
                       !l1_view(c, n, kComplex, inp, al2, 2, slots, partials, L.l1p, L.smem_l1p, L.grid_l1p) ||
-                      !l1_view(c, n, kComplex, int_, al2, 2, slots, partials, L.l1t, L.smem_l1t, L.grid_l1t,
+                      !l1_view(c, n, kComplex, int_, al2, 2, slots, partials1, L.l1t, L.smem_l1t, L.grid_l1t,
                                (int)sizeof(cplx2)) ||
-                      !l1_view(c, n, kReal, inr, al2, 2, slots, partials, L.l1r, L.smem_l1r, L.grid_l1r)))
+                      !l1_view(c, n, kReal, inr, al2, 2, slots, partials1, L.l1r, L.smem_l1r, L.grid_l1r)))
             throw ZkError{ZK_ERR_CUDA, "level-1 engine geometry"};
     }
     set_attrs(L);
@@ -940,11 +946,12 @@ DistSolver* dist_create(zk_context* c, zk_csr* A, int64_t n_halo, int64_t nnz_gl
     B.ph = jacobi ? vec() : B.p;
     B.sh = jacobi ? vec() : B.s;
     const int64_t pb = maxb > B.nblocks ? maxb : B.nblocks;
-    B.partials = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)(pb ? pb : 1)));
-    ZK_CUDA(cudaMemsetAsync(B.partials, 0, sizeof(double) * 4 * (size_t)(pb ? pb : 1), c->stream));
+    B.pslot = 4 * (pb ? pb : 1);
+    B.partials = static_cast<double*>(c->alloc.alloc(sizeof(double) * 2 * (size_t)B.pslot));
+    ZK_CUDA(cudaMemsetAsync(B.partials, 0, sizeof(double) * 2 * (size_t)B.pslot, c->stream));
     B.hist = static_cast<double*>(c->alloc.alloc(sizeof(double) * P->hist_cap));
     B.st = static_cast<SolverState*>(c->alloc.alloc(sizeof(SolverState)));
-    D->gathered = static_cast<double*>(c->alloc.alloc(sizeof(double) * 4 * (size_t)nranks * (size_t)(maxb ? maxb : 1)));
+    D->gathered = static_cast<double*>(c->alloc.alloc(sizeof(double) * 2 * (size_t)B.pslot * (size_t)nranks));
     D->P = P;
     D->L = make_launch(c, A, P);
     return D;
@@ -965,8 +972,8 @@ void* dist_vector(DistSolver* D, int which, int64_t* len) {
         case ZK_DVEC_SHAT: *len = D->n_ext; return B.sh;
         case ZK_DVEC_B: *len = D->n; return B.b;
         case ZK_DVEC_MINV: *len = B.jacobi ? D->n : 0; return B.minv;
-        case ZK_DVEC_PARTIALS: *len = 4 * (D->maxb > B.nblocks ? D->maxb : B.nblocks); return B.partials;
-        case ZK_DVEC_GATHERED: *len = 4 * (int64_t)D->nranks * D->maxb; return D->gathered;
+        case ZK_DVEC_PARTIALS: *len = 2 * B.pslot; return B.partials;
+        case ZK_DVEC_GATHERED: *len = 2 * B.pslot * (int64_t)D->nranks; return D->gathered;
         default: throw ZkError{ZK_ERR_PARAMETER, "unknown shard vector"};
     }
 }
@@ -1014,7 +1021,12 @@ void dist_phase(DistSolver* D, int phase) {
             k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t);
             break;
         case ZK_DPHASE_XR_UPDATE: k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); break;
-        case ZK_DPHASE_TRUE_RES: k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
+        case ZK_DPHASE_TRUE_RES:  // A x into t, residual pass -> slot 1
+            k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st);
+            ZK_CUDA(cudaGetLastError());
+            D->c->launches++;
+            k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r);
+            break;
         case ZK_DPHASE_P_NEXT: k_p_next<<<L.ew, 256, 0, s>>>(B); break;
         default: throw ZkError{ZK_ERR_PARAMETER, "unknown solver phase"};
     }
@@ -1028,17 +1040,18 @@ void dist_finish(DistSolver* D, int phase, const int64_t* rank_blocks) {
     for (int r = 0; r < D->nranks; ++r) rc.n[r] = rank_blocks[r];
     SolverBufs& B = D->P->bufs;
     cudaStream_t s = D->c->stream;
-    const double* g = D->gathered;
     const int nr = D->nranks;
-    const int64_t mb = D->maxb;
+    const int64_t rs = 2 * B.pslot;                        // doubles per rank in `gathered`
+    const double* g0 = D->gathered;                         // slot 0
+    const double* g1 = D->gathered + B.pslot;               // slot 1 (K4, K61)
     switch (phase) {
-        case ZK_DPHASE_SETUP: k_fold_finish<<<1, 32, 0, s>>>(SetupBody{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_PIVOT: k_fold_finish<<<1, 32, 0, s>>>(PivotFin{B, 0, 0}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_S_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(SUpdFinish{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_TRUE_RES_S: k_fold_finish<<<1, 32, 0, s>>>(ResBody<0>{B}, g, nr, mb, rc, 1); break;
-        case ZK_DPHASE_SPMV_T: k_fold_finish<<<1, 32, 0, s>>>(TFin{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_XR_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(XrFinish{B}, g, nr, mb, rc, 0); break;
-        case ZK_DPHASE_TRUE_RES: k_fold_finish<<<1, 32, 0, s>>>(ResBody<1>{B}, g, nr, mb, rc, 0); break;
+        case ZK_DPHASE_SETUP: k_fold_finish<<<1, 32, 0, s>>>(SetupBody{B}, g0, nr, rs, rc, 0); break;
+        case ZK_DPHASE_PIVOT: k_fold_finish<<<1, 32, 0, s>>>(PivotFin{B, 0, 0}, g0, nr, rs, rc, 0); break;
+        case ZK_DPHASE_S_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(SUpdFinish{B}, g0, nr, rs, rc, 0); break;
+        case ZK_DPHASE_TRUE_RES_S: k_fold_finish<<<1, 32, 0, s>>>(ResBody<0>{B}, g0, nr, rs, rc, 1); break;
+        case ZK_DPHASE_SPMV_T: k_fold_finish<<<1, 32, 0, s>>>(TFin{B}, g1, nr, rs, rc, 0); break;
+        case ZK_DPHASE_XR_UPDATE: k_fold_finish<<<1, 32, 0, s>>>(XrFinish{B}, g0, nr, rs, rc, 0); break;
+        case ZK_DPHASE_TRUE_RES: k_fold_finish<<<1, 32, 0, s>>>(ResBody<1>{B}, g1, nr, rs, rc, 0); break;
         default: throw ZkError{ZK_ERR_PARAMETER, "phase has no reduction"};
     }
     ZK_CUDA(cudaGetLastError());

@@ -50,7 +50,6 @@ BLOCK = 4096  # vecops.DEFAULT_PLAN.block_size: rank boundaries must be multiple
 DVEC_X, DVEC_PHAT, DVEC_SHAT, DVEC_B, DVEC_MINV, DVEC_PARTIALS, DVEC_GATHERED = range(7)
 (PH_SETUP, PH_P_FIRST, PH_PIVOT, PH_S_UPDATE, PH_X_ALPHA, PH_TRUE_RES_S, PH_SPMV_T, PH_XR_UPDATE,
  PH_TRUE_RES, PH_P_NEXT) = range(10)
-_NP = {PH_SETUP: 4, PH_PIVOT: 2, PH_S_UPDATE: 1, PH_TRUE_RES_S: 1, PH_SPMV_T: 4, PH_XR_UPDATE: 2, PH_TRUE_RES: 1}
 
 
 # ---- host-side planning (pure numpy; covered by the gloo tests on CPU) -------
@@ -156,11 +155,31 @@ class NcclTransport:
         import torch
         return torch.cuda.stream(self.stream)
 
-    def gather_partials(self, shard, np_):
-        n = shard.maxb * np_
+    def gather_partials(self, shard):
+        n = shard.partials_len
         src = _dev_tensor(shard.vec_ptr(DVEC_PARTIALS), n)
         dst = _dev_tensor(shard.vec_ptr(DVEC_GATHERED), n * shard.world)
         self.dist.all_gather_into_tensor(dst, src, group=self.group)
+
+    def gather_x(self, shard):
+        """The whole solution, all-gathered on the devices (rows padded to the
+        largest shard), as a device-resident ZVector."""
+        import torch
+        from .vecops import ZVector
+        nmax = int(np.diff(shard.bounds).max())
+        with self.ordered():
+            src = torch.zeros(2 * nmax, dtype=torch.float64, device=f"cuda:{torch.cuda.current_device()}")
+            src[: 2 * shard.n].copy_(_dev_tensor(shard.vec_ptr(DVEC_X), 2 * shard.n))
+            dst = torch.empty(2 * nmax * shard.world, dtype=src.dtype, device=src.device)
+            self.dist.all_gather_into_tensor(dst, src, group=self.group)
+            n = int(shard.bounds[-1])
+            x = ZVector._device_new(n)
+            out = _dev_tensor(x._dptr_out(), 2 * n)
+            for q in range(shard.world):
+                a, b = int(shard.bounds[q]), int(shard.bounds[q + 1])
+                out[2 * a: 2 * b].copy_(dst[2 * q * nmax: 2 * q * nmax + 2 * (b - a)])
+        self.stream.synchronize()
+        return x._written()
 
     def halo(self, shard, which):
         plan = shard.plan
@@ -191,9 +210,17 @@ class HostTransport:
         import contextlib
         return contextlib.nullcontext()
 
-    def gather_partials(self, shard, np_):
+    def gather_x(self, shard):
+        from .vecops import ZVector
+        x = np.empty(shard.n, dtype=np.complex128)
+        _lib.check(_lib.lib().zk_memcpy_d2h(_lib.context(), x.ctypes.data, shard.vec_ptr(DVEC_X), 16 * shard.n))
+        parts = [None] * shard.world
+        self.dist.all_gather_object(parts, x, group=self.group)
+        return ZVector(np.concatenate(parts))
+
+    def gather_partials(self, shard):
         import torch
-        n = shard.maxb * np_
+        n = shard.partials_len
         mine = np.empty(n, dtype=np.float64)
         _lib.check(_lib.lib().zk_memcpy_d2h(_lib.context(), mine.ctypes.data, shard.vec_ptr(DVEC_PARTIALS), 8 * n))
         parts = [torch.empty(n, dtype=torch.float64) for _ in range(shard.world)]
@@ -278,12 +305,15 @@ class ShardedBiCGStab:
             _lib.check(lib.zk_memcpy_h2d(_lib.context(), ib.ptr, arr.ctypes.data, 8 * len(idx)))
             self._send[q] = (ib, _lib.DeviceBuffer(16 * len(idx)), len(idx))
         self.transport = NcclTransport(group) if transport == "nccl" else HostTransport(group)
-        # NCCL: replay a captured iteration.  Verified at one rank; with peers
-        # the capture includes NCCL point-to-point ops, so it is opt-in there
-        # (ZK_DIST_GRAPH=1; =0 forces op-by-op issue everywhere).
+        n_part = ctypes.c_int64()
+        d = ctypes.POINTER(ctypes.c_double)()
+        _lib.check(lib.zk_dshard_vector(self._h, DVEC_PARTIALS, ctypes.byref(d), ctypes.byref(n_part)))
+        self.partials_len = int(n_part.value)  # two slots: two reductions per all-gather
+        # NCCL: one CUDA graph per iteration (kernels, halo send/recv and
+        # all-gathers on libzk's stream), replayed with one host launch;
+        # ZK_DIST_GRAPH=0 issues op by op (and capture failures fall back).
         import os
-        flag = os.environ.get("ZK_DIST_GRAPH")
-        self.use_graph = transport == "nccl" and (flag == "1" or (flag is None and self.world == 1))
+        self.use_graph = transport == "nccl" and os.environ.get("ZK_DIST_GRAPH") != "0"
         self._graph = None
 
     def __del__(self):
@@ -317,10 +347,13 @@ class ShardedBiCGStab:
     def _phase(self, ph: int) -> None:
         _lib.check(_lib.lib().zk_dshard_phase(self._h, ph))
 
+    def _finish(self, ph: int) -> None:
+        _lib.check(_lib.lib().zk_dshard_finish(self._h, ph, self.rank_blocks.ctypes.data))
+
     def _reduce(self, ph: int) -> None:
         self._phase(ph)
-        self.transport.gather_partials(self, _NP[ph])
-        _lib.check(_lib.lib().zk_dshard_finish(self._h, ph, self.rank_blocks.ctypes.data))
+        self.transport.gather_partials(self)
+        self._finish(ph)
 
     def _status(self):
         rep, done = _lib.SolveReportC(), ctypes.c_int32()
@@ -328,18 +361,29 @@ class ShardedBiCGStab:
         return rep, done.value
 
     def _iteration(self) -> None:
-        """One loop iteration (krylov.py:254-294) in the order of the 1-GPU
-        graph; every call is a device-side no-op once the solve stopped."""
+        """One loop iteration (krylov.py:254-294); every call is a device-side
+        no-op once the solve stopped.  Four all-gathers and four halo
+        exchanges: the s-check path's residual (K6x) is gathered with K4's
+        <t,t>, <t,s>, and K5's <r~,r> with K61's residual (two partials slots;
+        K4 / K61 run speculatively and their finishes are skipped when the
+        preceding finish stopped the solve), then finished in the reference's
+        order."""
         T = self.transport
         self._reduce(PH_S_UPDATE)
         self._phase(PH_X_ALPHA)
         T.halo(self, DVEC_X)
-        self._reduce(PH_TRUE_RES_S)
+        self._phase(PH_TRUE_RES_S)
         T.halo(self, DVEC_SHAT)
-        self._reduce(PH_SPMV_T)
-        self._reduce(PH_XR_UPDATE)
+        self._phase(PH_SPMV_T)
+        T.gather_partials(self)
+        self._finish(PH_TRUE_RES_S)
+        self._finish(PH_SPMV_T)
+        self._phase(PH_XR_UPDATE)
         T.halo(self, DVEC_X)
-        self._reduce(PH_TRUE_RES)
+        self._phase(PH_TRUE_RES)
+        T.gather_partials(self)
+        self._finish(PH_XR_UPDATE)
+        self._finish(PH_TRUE_RES)
         self._phase(PH_P_NEXT)
         T.halo(self, DVEC_PHAT)
         self._reduce(PH_PIVOT)
@@ -355,9 +399,10 @@ class ShardedBiCGStab:
 
     # -- the loop -----------------------------------------------------------------
     def solve(self, b_local, minv_local=None, x0_local=None, tolerance: float = 1e-9,
-              max_iterations: int = 1000, check_every: int = 8):
-        """Returns ``(x_local, SolveReport)``; raises BreakdownError like the
-        reference.  Identical reports on every rank."""
+              max_iterations: int = 1000, check_every: int = 8, gather: bool = False):
+        """Returns ``(x_local, SolveReport)`` -- or, with ``gather``, the whole
+        solution as a ZVector (device all-gather over NCCL) -- and raises
+        BreakdownError like the reference.  Identical reports on every rank."""
         if max_iterations > self.cap:
             raise ParameterError(f"max_iterations {max_iterations} above this shard's {self.cap}")
         t0 = time.perf_counter()
@@ -394,8 +439,12 @@ class ShardedBiCGStab:
         rep, done = self._status()
         hist = np.empty(rep.history_len, dtype=np.float64)
         _lib.check(lib.zk_dshard_history(self._h, hist.ctypes.data, rep.history_len))
-        x = np.zeros(self.n, dtype=np.complex128)
-        if done != 2:  # zero rhs: x = 0 (krylov.py:174-178)
+        if done == 2:  # zero rhs: x = 0 (krylov.py:174-178)
+            _lib.check(lib.zk_memset(_lib.context(), self.vec_ptr(DVEC_X), 0, 16 * self.n))
+        if gather:
+            x = self.transport.gather_x(self)
+        else:
+            x = np.empty(self.n, dtype=np.complex128)
             _lib.check(lib.zk_memcpy_d2h(_lib.context(), x.ctypes.data, self.vec_ptr(DVEC_X), 16 * self.n))
         history = [float(v) for v in hist]
         report = SolveReport(iterations=int(rep.iterations), final_relative_residual=history[-1],
@@ -412,7 +461,8 @@ def solve_bicgstab_sharded(A: CsrMatrix, b, M: Preconditioner | None = None, cfg
                            group=None, transport: str = "nccl"):
     """Row-sharded counterpart of :func:`krylov.solve_bicgstab` for one rank
     of ``group``: every rank passes the whole system and gets the whole
-    solution (all-gathered) and the same report."""
+    solution (a ZVector, all-gathered device to device over NCCL) and the
+    same report."""
     import torch.distributed as dist
     cfg = cfg or SolverConfig()
     n = A.n
@@ -431,9 +481,4 @@ def solve_bicgstab_sharded(A: CsrMatrix, b, M: Preconditioner | None = None, cfg
     guess = cfg.initial_guess
     x0 = None if guess is None else np.asarray(guess.data, dtype=np.complex128)[r0:r1]
     minv = M.data[r0:r1] if M.kind == "jacobi" else None
-    x_local, report = sh.solve(bvec[r0:r1], minv, x0, cfg.tolerance, cfg.max_iterations)
-    if world == 1:
-        return x_local, report
-    parts = [None] * world
-    dist.all_gather_object(parts, x_local, group=group)
-    return np.concatenate(parts), report
+    return sh.solve(bvec[r0:r1], minv, x0, cfg.tolerance, cfg.max_iterations, gather=True)

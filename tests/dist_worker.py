@@ -56,8 +56,9 @@ def solve_worker(rank, world, port, out, case, backend):
         transport = "nccl" if backend == "nccl" else "host"
         status, x, hist, it = "ok", np.zeros(0, np.complex128), [], -1
         try:
-            x, rep = D.solve_bicgstab_sharded(A, Z.ZVector(b), M, cfg, transport=transport)
-            hist, it = rep.residual_history, rep.iterations
+            xv, rep = D.solve_bicgstab_sharded(A, Z.ZVector(b), M, cfg, transport=transport)
+            assert isinstance(xv, Z.ZVector)
+            x, hist, it = xv.data, rep.residual_history, rep.iterations
         except Z.BreakdownError as e:
             status, hist, it = "breakdown", e.report.residual_history, e.report.iterations
         np.savez(os.path.join(out, f"rank{rank}.npz"), x=x, hist=np.asarray(hist), it=it, status=status)

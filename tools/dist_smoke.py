@@ -32,7 +32,7 @@ def main():
     O.set_arith(True, 262144)
     xo, hist, it, st, _ = O.bicgstab(n, ia, ja, aa, b, M.data, None, 1e-8, 400)
     print(f"rank {rank}: it {rep.iterations} (oracle {it}) hist_equal {rep.residual_history == hist} "
-          f"x_equal {x.tobytes() == xo.tobytes()}", flush=True)
+          f"x_equal {x.data.tobytes() == xo.tobytes()}", flush=True)
     dist.destroy_process_group()
 
 
