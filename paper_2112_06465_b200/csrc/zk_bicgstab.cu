@@ -40,6 +40,7 @@ namespace zk {
 SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv);
 size_t pipe_smem_bytes(const SellView& v, size_t extra);
 unsigned pipe_grid(const zk_csr* A);
+unsigned plain_grid(const zk_csr* A, SellView& v);
 
 enum : int32_t { ST_RUNNING = 0, ST_CONVERGED = 1, ST_NOT_CONVERGED = 2, ST_BREAKDOWN = 3 };
 enum : int32_t { BD_NONE = 0, BD_RHO = 1, BD_OMEGA = 2, BD_PIVOT = 3, BD_TT = 4 };
@@ -531,7 +532,8 @@ struct Launch {
     size_t smem_s, smem_r;
     RedCfg red, red1;          // reducer-warp SpMV kernels: partials slot 0 / slot 1 (row-sharded)
     PlanPtrs pc, pr;
-    unsigned nb, ew, pg;      // blocks, elementwise grid, SpMV grid
+    unsigned nb, ew, pg;      // blocks, elementwise grid, fused-reduction SpMV grid
+    unsigned ppg = 1;         // plain SpMV grid (pipeline blocks may be smaller than 4096 rows)
     RankCounts one;           // {nblocks}: the 1-GPU fold's partial count
     // K3 / K5 and the K2 / K4 reduction passes on the TMA-fed engine (zk_l1pipe.cuh)
     L1View l1s, l1x, l1p, l1t;
@@ -589,7 +591,7 @@ void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr)
     SolverBufs B = L.P->bufs;
     { PhaseScope ps(pe, PH_SETUP); k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); }
     { PhaseScope ps(pe, PH_P_FIRST); k_p_first<<<L.ew, 256, 0, s>>>(B); }
-    { PhaseScope ps(pe, PH_PIVOT_FIRST); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
+    { PhaseScope ps(pe, PH_PIVOT_FIRST); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
     { PhaseScope ps(pe, PH_PIVOT_FIRST_DOT); k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0); }
 }
 constexpr int kPrologueKernels = 4;
@@ -604,26 +606,26 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     { PhaseScope ps(pe, PH_S_UPDATE); k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s); }
     { PhaseScope ps(pe, PH_X_ALPHA); k_x_alpha<<<L.ew, 256, 0, s>>>(B); }
     { PhaseScope ps(pe, PH_TRUE_RES_S); k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); }
-    { PhaseScope ps(pe, PH_SPMV_T); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st); }
+    { PhaseScope ps(pe, PH_SPMV_T); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st); }
     { PhaseScope ps(pe, PH_TT_TS); k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t); }
     { PhaseScope ps(pe, PH_XR_UPDATE); k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); }
     if (L.fuse2) {
         { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
         {
             PhaseScope ps(pe, PH_SPMV2);
-            k_spmv2_phase<<<L.pg, kPipeThreads, L.smem_pl2, s>>>(L.Apl2, B.x, B.ph, B.t, B.v, B.st);
+            k_spmv2_phase<<<L.ppg, kPipeThreads, L.smem_pl2, s>>>(L.Apl2, B.x, B.ph, B.t, B.v, B.st);
         }
         { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
     } else {
         if (L.respass) {  // K61 as a plain SpMV into t + the residual pass
-            { PhaseScope ps(pe, PH_TRUE_RES); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st); }
+            { PhaseScope ps(pe, PH_TRUE_RES); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st); }
             { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
         } else {
             PhaseScope ps(pe, PH_TRUE_RES);
             k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
         }
         { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
-        { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
+        { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
     }
     {
         PhaseScope ps(pe, PH_PIVOT_DOT);
@@ -760,6 +762,8 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.Ar.sv[0] = B.b;
     L.Apl = sell_view(A, c, 0, 0);
     L.Apl2 = sell_view(A, c, 0, 0);
+    L.ppg = plain_grid(A, L.Apl);
+    plain_grid(A, L.Apl2);
     {
         // one matrix pass for K61 + K2 measured slower on C4 (1703 us vs 799 +
         // 716 us: two gathered vectors make the consumers the bottleneck);
@@ -1006,7 +1010,7 @@ void dist_phase(DistSolver* D, int phase) {
         case ZK_DPHASE_SETUP: k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); break;
         case ZK_DPHASE_P_FIRST: k_p_first<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_PIVOT:
-            k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
+            k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
             ZK_CUDA(cudaGetLastError());
             D->c->launches++;
             k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0);
@@ -1015,14 +1019,14 @@ void dist_phase(DistSolver* D, int phase) {
         case ZK_DPHASE_X_ALPHA: k_x_alpha<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_TRUE_RES_S: k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_SPMV_T:
-            k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st);
+            k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st);
             ZK_CUDA(cudaGetLastError());
             D->c->launches++;
             k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t);
             break;
         case ZK_DPHASE_XR_UPDATE: k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); break;
         case ZK_DPHASE_TRUE_RES:  // A x into t, residual pass -> slot 1
-            k_spmv_phase<<<L.pg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st);
+            k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st);
             ZK_CUDA(cudaGetLastError());
             D->c->launches++;
             k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r);

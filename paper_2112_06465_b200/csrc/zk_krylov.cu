@@ -39,6 +39,7 @@ namespace zk {
 SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv);
 size_t pipe_smem_bytes(const SellView& v, size_t extra);
 unsigned pipe_grid(const zk_csr* A);
+unsigned plain_grid(const zk_csr* A, SellView& v);
 double* fold_slots(zk_context* c, int64_t count);
 void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, bool conj, int64_t block, int mode,
                  double2* result, Gate gate);
@@ -540,10 +541,11 @@ struct KLaunch {
         check();
     }
     void spmv(const double2* x, double2* y, double2* y2, Gate g) {
-        const SellView v = sell_view(A, c, 0, 0);
+        SellView v = sell_view(A, c, 0, 0);
+        const unsigned grid = plain_grid(A, v);
         const size_t smem = pipe_smem_bytes(v, 0);
         ZK_CUDA(cudaFuncSetAttribute(k_kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_kspmv<<<pg, kPipeThreads, smem, s>>>(v, x, KPlainBody{y, y2}, g);
+        k_kspmv<<<grid, kPipeThreads, smem, s>>>(v, x, KPlainBody{y, y2}, g);
         check();
     }
     // op(v) = spmv(A, M.apply(v)) into out; identity M.apply is a copy (bitwise v)

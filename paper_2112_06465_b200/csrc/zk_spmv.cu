@@ -59,6 +59,8 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) 
         v.swap = (A->nnz_elide * 16 >= c->elide_bytes);
         v.fma = c->fma != 0;
         v.ns_magic = (uint32_t)((1ull << 32) / (uint64_t)v.ns + 1);
+        v.spb = kBlock / kSlice;
+        v.nvb = A->nblocks;
         return v;
     }
     for (int cm = cm_hi; cm >= cm_lo; --cm) {
@@ -78,6 +80,8 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) 
     v.swap = (A->nnz_elide * 16 >= c->elide_bytes);
     v.fma = c->fma != 0;
     v.ns_magic = (uint32_t)((1ull << 32) / (uint64_t)v.ns + 1);
+    v.spb = kBlock / kSlice;
+    v.nvb = A->nblocks;
     return v;
 }
 
@@ -87,6 +91,22 @@ size_t pipe_smem_bytes(const SellView& v, size_t extra) {
 
 unsigned pipe_grid(const zk_csr* A) {
     int64_t g = A->nblocks < num_sms() ? A->nblocks : num_sms();
+    return (unsigned)(g > 0 ? g : 1);
+}
+
+// Plain (reduction-free) SpMV launches: pipeline blocks of v.spb slices --
+// 128 (the 4096-row block) for large matrices, fewer when the matrix has
+// fewer blocks than two per SM, so every SM streams -- and its grid.
+unsigned plain_grid(const zk_csr* A, SellView& v) {
+    const int64_t want = 2 * (int64_t)num_sms();
+    int64_t spb = kBlock / kSlice;
+    if (A->nslices < want * spb) {
+        spb = (A->nslices + want - 1) / want;
+        if (spb < 4) spb = 4;
+    }
+    v.spb = (int32_t)spb;
+    v.nvb = (A->nslices + spb - 1) / spb;
+    const int64_t g = v.nvb < num_sms() ? v.nvb : num_sms();
     return (unsigned)(g > 0 ? g : 1);
 }
 
@@ -354,10 +374,11 @@ void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
         ZK_CUDA(cudaMemsetAsync(y, 0, sizeof(double2) * A->n_rows, c->stream));
         return;
     }
-    const SellView v = sell_view(A, c, 0, 0);
+    SellView v = sell_view(A, c, 0, 0);
+    const unsigned grid = plain_grid(A, v);
     const size_t smem = pipe_smem_bytes(v, 0);
     ZK_CUDA(cudaFuncSetAttribute(k_spmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_spmv<<<pipe_grid(A), kPipeThreads, smem, c->stream>>>(v, x, y);
+    k_spmv<<<grid, kPipeThreads, smem, c->stream>>>(v, x, y);
     ZK_CUDA(cudaGetLastError());
     c->launches++;
 }

@@ -93,6 +93,11 @@ struct SellView {
     const double2* sv[2]; // their base pointers (row-indexed, n_rows long)
     int32_t ns;           // ring stages for this launch
     uint32_t ns_magic;    // floor(2^32 / ns) + 1: i / ns = umulhi(i, ns_magic) for i < 2^27
+    // plain (reduction-free) pipelines may cut the rows into smaller
+    // pipeline blocks of `spb` slices (nvb of them), so a small matrix still
+    // spreads over every SM; fused-reduction pipelines keep 4096-row blocks
+    int32_t spb;
+    int64_t nvb;
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
 };
@@ -232,54 +237,108 @@ struct RowAcc {
     }
 };
 
+// ---- long rows (> 65 entries, side CSR): one WARP per row ----------------------
+// numpy's CDOUBLE_pairwise_sum over the products [s, s+L) of a long row: the
+// recursion halves a range (split at (L - L%8)/2) until it holds <= 64
+// elements, a leaf sums with four lane accumulators over full groups of
+// four, (l0+l1)+(l2+l3), then its leftovers.  The warp walks the recursion in
+// lockstep (every lane the same explicit stack, so control flow is uniform);
+// each subtree of <= kLongChunk elements (<= 32 leaves) is a CHUNK whose
+// leaves are summed one per lane in parallel and combined in the recursion's
+// order through shuffles.  Every lane ends with the row value.
+constexpr int64_t kLongChunk = 896;  // leaves are >= 28 elements: <= 32 leaves per chunk
+
 __device__ __forceinline__ double2 long_prod(const SellView& A, const double2* __restrict__ x, int64_t idx) {
     return spmv_prod(A, A.long_aa[idx], __ldg(x + A.long_ja[idx]));
 }
 
-// numpy CDOUBLE_pairwise_sum over products [s, s+L) of the side CSR,
-// evaluated iteratively (explicit post-order stack; no device recursion, so
-// the calling kernels keep their register allocation).
-static __device__ __noinline__ double2 long_pw(const SellView A, const double2* __restrict__ x, int64_t s, int64_t L) {
-    int64_t fs[40], fl[40];
-    int8_t fphase[40];
-    double2 vals[40];
-    int sp = 0, vp = 0;
-    fs[0] = s;
-    fl[0] = L;
-    fphase[0] = 0;
-    sp = 1;
+__device__ __forceinline__ int64_t pw_split(int64_t L) { return (L - L % 8) / 2; }
+
+// One numpy leaf (L <= 64) of products [s, s+L), summed by one thread.
+__device__ __forceinline__ double2 long_leaf(const SellView& A, const double2* __restrict__ x, int64_t s, int64_t L) {
+    if (L < 4) {
+        double2 acc = make_double2(-0.0, -0.0);
+        for (int64_t k = 0; k < L; ++k) acc = cadd(acc, long_prod(A, x, s + k));
+        return acc;
+    }
+    double2 r0 = long_prod(A, x, s), r1 = long_prod(A, x, s + 1), r2 = long_prod(A, x, s + 2), r3 = long_prod(A, x, s + 3);
+    const int64_t G = L / 4;
+    for (int64_t g = 1; g < G; ++g) {
+        const double2 p0 = long_prod(A, x, s + 4 * g), p1 = long_prod(A, x, s + 4 * g + 1);
+        const double2 p2 = long_prod(A, x, s + 4 * g + 2), p3 = long_prod(A, x, s + 4 * g + 3);
+        r0 = cadd(r0, p0);
+        r1 = cadd(r1, p1);
+        r2 = cadd(r2, p2);
+        r3 = cadd(r3, p3);
+    }
+    double2 acc = cadd(cadd(r0, r1), cadd(r2, r3));
+    for (int64_t k = 4 * G; k < L; ++k) acc = cadd(acc, long_prod(A, x, s + k));
+    return acc;
+}
+
+// A chunk [s, s+L) (L <= kLongChunk): lane i sums leaf i, then the chunk's
+// tree is combined in recursion order (all lanes, shuffles).
+__device__ __noinline__ double2 long_chunk(const SellView A, const double2* __restrict__ x, int64_t s, int64_t L) {
+    const int lane = threadIdx.x & 31;
+    if (L <= 64) {  // a single leaf: lane 0 sums it
+        double2 v = make_double2(0.0, 0.0);
+        if (lane == 0) v = long_leaf(A, x, s, L);
+        return make_double2(__shfl_sync(0xffffffffu, v.x, 0), __shfl_sync(0xffffffffu, v.y, 0));
+    }
+    // pass 1: enumerate leaves in order; lane i keeps leaf i
+    int64_t st[8], ln[8];
+    int8_t ph[8];
+    int sp = 1, nleaf = 0;
+    int64_t my_s = 0, my_l = 0;
+    st[0] = s;
+    ln[0] = L;
+    ph[0] = 0;
     while (sp > 0) {
-        const int64_t cs = fs[sp - 1], cl = fl[sp - 1];
-        if (cl <= 64) {  // leaf
-            double2 acc;
-            if (cl < 4) {
-                acc = make_double2(-0.0, -0.0);
-                for (int64_t k = 0; k < cl; ++k) acc = cadd(acc, long_prod(A, x, cs + k));
-            } else {
-                double2 r0 = long_prod(A, x, cs), r1 = long_prod(A, x, cs + 1);
-                double2 r2 = long_prod(A, x, cs + 2), r3 = long_prod(A, x, cs + 3);
-                const int64_t G = cl / 4;
-                for (int64_t g = 1; g < G; ++g) {
-                    r0 = cadd(r0, long_prod(A, x, cs + 4 * g));
-                    r1 = cadd(r1, long_prod(A, x, cs + 4 * g + 1));
-                    r2 = cadd(r2, long_prod(A, x, cs + 4 * g + 2));
-                    r3 = cadd(r3, long_prod(A, x, cs + 4 * g + 3));
-                }
-                acc = cadd(cadd(r0, r1), cadd(r2, r3));
-                for (int64_t k = 4 * G; k < cl; ++k) acc = cadd(acc, long_prod(A, x, cs + k));
+        const int64_t cs = st[sp - 1], cl = ln[sp - 1];
+        if (cl <= 64) {
+            if (nleaf == lane) {
+                my_s = cs;
+                my_l = cl;
             }
-            vals[vp++] = acc;
+            ++nleaf;
             --sp;
             continue;
         }
-        const int64_t h = (cl - cl % 8) / 2;
-        if (fphase[sp - 1] == 0) {  // descend left
-            fphase[sp - 1] = 1;
-            fs[sp] = cs; fl[sp] = h; fphase[sp] = 0; ++sp;
-        } else if (fphase[sp - 1] == 1) {  // descend right
-            fphase[sp - 1] = 2;
-            fs[sp] = cs + h; fl[sp] = cl - h; fphase[sp] = 0; ++sp;
-        } else {  // both halves done: combine left + right
+        const int64_t h = pw_split(cl);
+        if (ph[sp - 1] == 0) {
+            ph[sp - 1] = 1;
+            st[sp] = cs; ln[sp] = h; ph[sp] = 0; ++sp;
+        } else if (ph[sp - 1] == 1) {
+            ph[sp - 1] = 2;
+            st[sp] = cs + h; ln[sp] = cl - h; ph[sp] = 0; ++sp;
+        } else {
+            --sp;
+        }
+    }
+    const double2 leaf = lane < nleaf ? long_leaf(A, x, my_s, my_l) : make_double2(0.0, 0.0);
+    // pass 2: post-order combine, leaf values fetched from their lanes
+    double2 vals[8];
+    int vp = 0, li = 0;
+    sp = 1;
+    st[0] = s;
+    ln[0] = L;
+    ph[0] = 0;
+    while (sp > 0) {
+        const int64_t cs = st[sp - 1], cl = ln[sp - 1];
+        if (cl <= 64) {
+            vals[vp++] = make_double2(__shfl_sync(0xffffffffu, leaf.x, li), __shfl_sync(0xffffffffu, leaf.y, li));
+            ++li;
+            --sp;
+            continue;
+        }
+        const int64_t h = pw_split(cl);
+        if (ph[sp - 1] == 0) {
+            ph[sp - 1] = 1;
+            st[sp] = cs; ln[sp] = h; ph[sp] = 0; ++sp;
+        } else if (ph[sp - 1] == 1) {
+            ph[sp - 1] = 2;
+            st[sp] = cs + h; ln[sp] = cl - h; ph[sp] = 0; ++sp;
+        } else {
             const double2 b = vals[--vp];
             const double2 a = vals[--vp];
             vals[vp++] = cadd(a, b);
@@ -289,10 +348,41 @@ static __device__ __noinline__ double2 long_pw(const SellView A, const double2* 
     return vals[0];
 }
 
-__device__ __forceinline__ double2 long_row_sum(const SellView& A, const double2* __restrict__ x, int li) {
+// Row value of long row li: v0 + PW(v1 .. v_{L-1}); whole warp, uniform li.
+__device__ __noinline__ double2 long_row_warp(const SellView A, const double2* __restrict__ x, int li) {
     const int64_t lo = A.long_ia[li], L = A.long_ia[li + 1] - lo;
-    double2 v0 = long_prod(A, x, lo);
-    return cadd(v0, long_pw(A, x, lo + 1, L - 1));
+    const double2 v0 = long_prod(A, x, lo);
+    const int64_t s = lo + 1, n = L - 1;
+    // top of the recursion above the chunks (uniform explicit stack)
+    int64_t st[48], ln[48];
+    int8_t ph[48];
+    double2 vals[48];
+    int sp = 1, vp = 0;
+    st[0] = s;
+    ln[0] = n;
+    ph[0] = 0;
+    while (sp > 0) {
+        const int64_t cs = st[sp - 1], cl = ln[sp - 1];
+        if (cl <= kLongChunk) {
+            vals[vp++] = long_chunk(A, x, cs, cl);
+            --sp;
+            continue;
+        }
+        const int64_t h = pw_split(cl);
+        if (ph[sp - 1] == 0) {
+            ph[sp - 1] = 1;
+            st[sp] = cs; ln[sp] = h; ph[sp] = 0; ++sp;
+        } else if (ph[sp - 1] == 1) {
+            ph[sp - 1] = 2;
+            st[sp] = cs + h; ln[sp] = cl - h; ph[sp] = 0; ++sp;
+        } else {
+            const double2 b = vals[--vp];
+            const double2 a = vals[--vp];
+            vals[vp++] = cadd(a, b);
+            --sp;
+        }
+    }
+    return cadd(v0, vals[0]);
 }
 
 // ---- fast row path (whole slice per stage, FMA fingerprint) --------------
@@ -877,7 +967,10 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ns = A.ns, nch = A.nch;
     const int cols = 1 + 4 * A.cm;
-    constexpr int kSlicesPerBlock = kBlock / kSlice;
+    // pipeline block: the 4096-row reduction block for fused reductions,
+    // A.spb slices otherwise
+    const int kSlicesPerBlock = kRed ? kBlock / kSlice : A.spb;
+    const int64_t nblk = kRed ? A.nblocks : A.nvb;
     if (threadIdx.x == 0) {
         for (int i = 0; i < ns; ++i) {
             mbar_init(&full[i], 1);
@@ -916,14 +1009,15 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
             c = (int)(i % (uint32_t)nch);
             const int64_t blk = blockIdx.x + (int64_t)(seq / kSlicesPerBlock) * gridDim.x;
             s = blk * kSlicesPerBlock + (seq % kSlicesPerBlock);
-            active = blk < A.nblocks && s < A.nslices;
+            active = blk < nblk && s < A.nslices;
             if (active) {
                 off0 = __ldg(A.slice_off + s);
                 off1 = __ldg(A.slice_off + s + 1);
                 // leading edge of the x window: columns above the previous
                 // slice's largest (a block's first slice: the 4096 below its own)
                 cm_hi = __ldg(A.slice_cmax + s);
-                cm_lo = (s % kSlicesPerBlock != 0) ? __ldg(A.slice_cmax + s - 1) + 1 : cm_hi - (kBlock - 1);
+                cm_lo = (s % kSlicesPerBlock != 0) ? __ldg(A.slice_cmax + s - 1) + 1
+                                                   : cm_hi - (kSlicesPerBlock * kSlice - 1);
                 if (cm_lo < 0) cm_lo = 0;
             }
         };
@@ -972,7 +1066,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
     // ---- consumer warps: warp w takes slices w, w+kCW, ... of each block ----
     const bool fast = A.cm == 0 && A.fma;
     uint32_t sbase = 0;  // CTA-local index of the block's first slice
-    for (int64_t blk = blockIdx.x; blk < A.nblocks; blk += gridDim.x) {
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         const int64_t s_lo = blk * kSlicesPerBlock;
         const int64_t s_hi = (s_lo + kSlicesPerBlock < A.nslices) ? s_lo + kSlicesPerBlock : A.nslices;
         const int nsl = (int)(s_hi - s_lo);
@@ -1007,10 +1101,17 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
 #pragma unroll
                 for (int v = 0; v < SV; ++v) svals[v] = mine ? A.sv[v][row] : make_double2(0.0, 0.0);
             }
-            if (mine && len == 255) {  // long row: side CSR, full pairwise recursion
-                const int li = long_index(A, blk, row);
-                val.v[0] = long_row_sum(A, x0, li);
-                if constexpr (NX == 2) val.v[1] = long_row_sum(A, x1, li);
+            // long rows (side CSR): the whole warp sums each in turn
+            for (unsigned lm = __ballot_sync(0xffffffffu, mine && len == 255); lm; lm &= lm - 1) {
+                const int src = __ffs(lm) - 1;
+                const int64_t lrow = __shfl_sync(0xffffffffu, row, src);
+                const int li = long_index(A, lrow / kBlock, lrow);
+                const double2 r0 = long_row_warp(A, x0, li);
+                if (lane == src) val.v[0] = r0;
+                if constexpr (NX == 2) {
+                    const double2 r1 = long_row_warp(A, x1, li);
+                    if (lane == src) val.v[1] = r1;
+                }
             }
             double2 tc[NC > 0 ? NC : 1];
             double tr[NR > 0 ? NR : 1];

@@ -251,3 +251,29 @@ def test_wide_rows_stage_reuse(n, lo, hi):
         xs, rep = Z.solve_bicgstab(A, Z.ZVector(b), M, Z.SolverConfig(tolerance=1e-10, max_iterations=500))
         assert rep.residual_history == hist
         assert bits(xs.data) == bits(xo)
+
+
+@pytest.mark.parametrize("swap", [False, True])
+def test_long_rows_warp_path_vs_oracle(swap):
+    """Rows longer than 65 entries (side CSR, one warp per row): lengths
+    around the leaf / chunk / split boundaries and up to 60k entries, mixed
+    with short and empty rows in the same slices, both elision orders."""
+    rng = np.random.default_rng(2024)
+    n_rows, n_cols = 300, 70000
+    lens = rng.integers(0, 12, n_rows)
+    special = [66, 67, 129, 130, 200, 897, 898, 1793, 5000, 20001, 60000]
+    for k, L in enumerate(special):
+        lens[7 + 23 * k] = L
+    ia = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ja = np.concatenate([np.sort(rng.choice(n_cols, L, replace=False)) for L in lens]).astype(np.int64)
+    aa = rng.standard_normal(ia[-1]) + 1j * rng.standard_normal(ia[-1])
+    x = rng.standard_normal(n_cols) + 1j * rng.standard_normal(n_cols)
+    elide = 16 if swap else 1 << 62  # force numpy's elided (swapped) product order or not
+    Z.set_arithmetic(True, elide)
+    O.set_arith(True, elide)
+    try:
+        A = Z.CsrMatrix(n_rows, n_cols, aa, ja, ia)
+        assert bits(Z.spmv(A, Z.ZVector(x)).data) == bits(O.spmv(n_rows, n_cols, ia, ja, aa, x))
+    finally:
+        Z.set_arithmetic(True, 262144)
+        O.set_arith(True, 262144)
