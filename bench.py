@@ -316,8 +316,8 @@ def run_zk(args, dist: Dist):
         if p in conditional:
             continue
         k = kernel_names.get(p, p)
-        t, c_, b = per_kernel.get(k, (0.0, 0, 0))
-        per_kernel[k] = (t + prof[p][0], c_ + prof[p][1], b + B[p] * prof[p][1])
+        kt, kc, kb = per_kernel.get(k, (0.0, 0, 0))
+        per_kernel[k] = (kt + prof[p][0], kc + prof[p][1], kb + B[p] * prof[p][1])
     dominant = max(per_kernel, key=lambda k: per_kernel[k][0])
     dom_ms, dom_cnt, dom_bytes = per_kernel[dominant]
     dom_avg_s = dom_ms / dom_cnt / 1e3

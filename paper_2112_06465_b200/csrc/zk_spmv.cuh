@@ -278,7 +278,7 @@ __device__ __forceinline__ double2 long_leaf(const SellView& A, const double2* _
 
 // A chunk [s, s+L) (L <= kLongChunk): lane i sums leaf i, then the chunk's
 // tree is combined in recursion order (all lanes, shuffles).
-__device__ __noinline__ double2 long_chunk(const SellView A, const double2* __restrict__ x, int64_t s, int64_t L) {
+static __device__ __noinline__ double2 long_chunk(const SellView A, const double2* __restrict__ x, int64_t s, int64_t L) {
     const int lane = threadIdx.x & 31;
     if (L <= 64) {  // a single leaf: lane 0 sums it
         double2 v = make_double2(0.0, 0.0);
@@ -349,7 +349,7 @@ __device__ __noinline__ double2 long_chunk(const SellView A, const double2* __re
 }
 
 // Row value of long row li: v0 + PW(v1 .. v_{L-1}); whole warp, uniform li.
-__device__ __noinline__ double2 long_row_warp(const SellView A, const double2* __restrict__ x, int li) {
+static __device__ __noinline__ double2 long_row_warp(const SellView A, const double2* __restrict__ x, int li) {
     const int64_t lo = A.long_ia[li], L = A.long_ia[li + 1] - lo;
     const double2 v0 = long_prod(A, x, lo);
     const int64_t s = lo + 1, n = L - 1;
@@ -597,6 +597,27 @@ __device__ __forceinline__ int long_index(const SellView& A, int64_t blk, int64_
         else hi = mid;
     }
     return lo;
+}
+
+
+// The long rows of one slice (lanes in `lm`), one after the other, each by
+// the whole warp; the owning lane takes the row value.
+template <int NX>
+static __device__ __noinline__ void long_rows_slice(const SellView A, const double2* __restrict__ x0,
+                                                    const double2* __restrict__ x1, unsigned lm, int64_t row,
+                                                    RowVals<NX>& val) {
+    const int lane = threadIdx.x & 31;
+    for (; lm; lm &= lm - 1) {
+        const int src = __ffs(lm) - 1;
+        const int64_t lrow = __shfl_sync(0xffffffffu, row, src);
+        const int li = long_index(A, lrow / kBlock, lrow);
+        const double2 r0 = long_row_warp(A, x0, li);
+        if (lane == src) val.v[0] = r0;
+        if constexpr (NX == 2) {
+            const double2 r1 = long_row_warp(A, x1, li);
+            if (lane == src) val.v[1] = r1;
+        }
+    }
 }
 
 // Generic slice path (rows wider than kFullCols split over chunks, or the
@@ -1101,17 +1122,12 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
 #pragma unroll
                 for (int v = 0; v < SV; ++v) svals[v] = mine ? A.sv[v][row] : make_double2(0.0, 0.0);
             }
-            // long rows (side CSR): the whole warp sums each in turn
-            for (unsigned lm = __ballot_sync(0xffffffffu, mine && len == 255); lm; lm &= lm - 1) {
-                const int src = __ffs(lm) - 1;
-                const int64_t lrow = __shfl_sync(0xffffffffu, row, src);
-                const int li = long_index(A, lrow / kBlock, lrow);
-                const double2 r0 = long_row_warp(A, x0, li);
-                if (lane == src) val.v[0] = r0;
-                if constexpr (NX == 2) {
-                    const double2 r1 = long_row_warp(A, x1, li);
-                    if (lane == src) val.v[1] = r1;
-                }
+            // long rows (side CSR): the whole warp sums each in turn, out of
+            // line and only for matrices that have any (keeps the hot loop's
+            // registers and schedule)
+            if (A.long_blk_ptr != nullptr) {
+                const unsigned lm = __ballot_sync(0xffffffffu, mine && len == 255);
+                if (lm) long_rows_slice<NX>(A, x0, x1, lm, row, val);
             }
             double2 tc[NC > 0 ? NC : 1];
             double tr[NR > 0 ? NR : 1];
