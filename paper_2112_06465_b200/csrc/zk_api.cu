@@ -98,6 +98,8 @@ void zdot_device(zk_context* c, int64_t n, const double2* x, const double2* y, b
                  double2* result, Gate gate = Gate{nullptr, 0});
 void znorm2_device(zk_context* c, int64_t n, const double2* x, int64_t block, int mode, double* result,
                    Gate gate = Gate{nullptr, 0});
+zk_csr* build_sell_streamed(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
+                            const int64_t* ja_h, const double2* aa_h);
 zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
                    const int64_t* ia_d, const int64_t* ja_d, const double2* aa_d);
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y);
@@ -249,6 +251,9 @@ zk_status zk_context_destroy(zk_context* c) {
         if (c->bounce) cudaFreeHost(c->bounce);
         for (auto& e : c->bounce_ev)
             if (e) cudaEventDestroy(e);
+        for (auto& e : c->up_ev)
+            if (e) cudaEventDestroy(e);
+        if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
         cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -567,7 +572,7 @@ zk_status zk_znorm2(zk_context* c, int64_t n, const double* x, int64_t block_siz
     });
 }
 
-static void validate_csr_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia) {
+static void validate_csr_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia, bool monotone = true) {
     need(n_rows >= 0 && n_cols >= 0 && nnz >= 0, ZK_ERR_FORMAT, "negative dimensions");
     need(n_cols <= INT32_MAX, ZK_ERR_FORMAT, "n_cols exceeds the int32 column-index range of the device layout");
     if (n_rows == 0) {
@@ -576,7 +581,8 @@ static void validate_csr_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const
     }
     need(ia != nullptr, ZK_ERR_FORMAT, "null row pointers");
     need(ia[0] == 0 && ia[n_rows] == nnz, ZK_ERR_FORMAT, "row pointers must span [0, nnz]");
-    for (int64_t i = 0; i < n_rows; ++i) need(ia[i + 1] >= ia[i], ZK_ERR_FORMAT, "row pointers are not nondecreasing");
+    if (monotone)
+        for (int64_t i = 0; i < n_rows; ++i) need(ia[i + 1] >= ia[i], ZK_ERR_FORMAT, "row pointers are not nondecreasing");
     // column indices are range-checked on the device while scattering (zk_spmv.cu)
 }
 
@@ -585,12 +591,19 @@ zk_status zk_csr_create(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t n
     return guarded([&] {
         need_ctx(c);
         need(out != nullptr, ZK_ERR_PARAMETER, "null output");
-        validate_csr_host(n_rows, n_cols, nnz, ia_host);
+        validate_csr_host(n_rows, n_cols, nnz, ia_host, /*monotone=*/false);  // monotonicity: on the device
         need(nnz == 0 || (ja_host && aa_host), ZK_ERR_FORMAT, "null column/value arrays");
         std::vector<int64_t> ia0;
         if (n_rows == 0) {
             ia0.assign(1, 0);
             ia_host = ia0.data();
+        }
+        if (n_rows > 0 && nnz > 0) {  // pipelined upload + device layout build (zk_spmv.cu)
+            zk_csr* A = build_sell_streamed(c, n_rows, n_cols, nnz, ia_host, ja_host, D2(aa_host));
+            if (A) {
+                *out = A;
+                return;
+            }
         }
         int64_t* ia_d = static_cast<int64_t*>(c->alloc.alloc(sizeof(int64_t) * (n_rows + 1)));
         int64_t* ja_d = static_cast<int64_t*>(c->alloc.alloc(sizeof(int64_t) * (nnz ? nnz : 1)));

@@ -84,6 +84,8 @@ struct zk_csr {
 struct zk_context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // matrix upload pipeline (zk_spmv.cu build_sell_streamed)
+    cudaEvent_t up_ev[4] = {};
     zk::Allocator alloc;
     std::map<std::pair<int32_t, int32_t>, char*> plans;  // (L, kind) -> device plan
     int fma = 1;

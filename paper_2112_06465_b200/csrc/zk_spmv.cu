@@ -4,6 +4,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "zk_internal.h"
 #include "zk_spmv.cuh"
 
@@ -155,6 +157,52 @@ __global__ void k_long_scatter(int32_t n_long, int64_t n_cols, const int32_t* __
     }
     if (!ok) atomicOr(bad, 1u);
     if (len > 0 && ok) atomicMax(cmax + long_row[li] / kSlice, (int32_t)ja[lo + len - 1]);
+}
+
+// ---- streamed upload: host CSR -> SELL-32 with the H2D copies pipelined ------
+// Row lengths, slice widths and the monotonicity check of the row pointers
+// on the device (one thread per row; slice width = widest short row).
+__global__ void k_rowinfo(int64_t n_rows, const int64_t* __restrict__ ia, uint8_t* __restrict__ rowlen,
+                          int64_t* __restrict__ swidth, unsigned long long* info) {
+    const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    int64_t len = 0;
+    if (row < n_rows) {
+        len = ia[row + 1] - ia[row];
+        if (len < 0) atomicOr(info + 0, 1ull);  // row pointers decrease
+        if (len > kShortMax) atomicAdd(info + 1, 1ull);
+        rowlen[row] = len > kShortMax ? 255 : (uint8_t)(len < 0 ? 0 : len);
+    }
+    int64_t w = (row < n_rows && len >= 0 && len <= kShortMax) ? len : 0;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) w = max(w, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)w, d));
+    if (lane == 0 && row - lane < n_rows) {
+        swidth[row / kSlice] = (int64_t)kSlice * w;
+        atomicMax(info + 2, (unsigned long long)w);
+    }
+}
+
+// Scatter rows [r0, r1) whose entries sit in the staging buffers (entry k of
+// the matrix at index k - nz0).
+__global__ void k_sell_scatter_chunk(int64_t r0, int64_t r1, int64_t n_cols, const int64_t* __restrict__ ia,
+                                     int64_t nz0, const int64_t* __restrict__ ja, const double2* __restrict__ aa,
+                                     const int64_t* __restrict__ slice_off, const uint8_t* __restrict__ rowlen,
+                                     double2* __restrict__ saa, int32_t* __restrict__ sja, int32_t* __restrict__ cmax,
+                                     unsigned int* bad) {
+    const int64_t row = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= r1) return;
+    const int len = rowlen[row];
+    const int64_t base = slice_off[row / kSlice] + (row % kSlice);
+    const int64_t lo = ia[row] - nz0;
+    bool ok = true;
+    for (int k = 0; k < len; ++k) {
+        const int64_t j = ja[lo + k];
+        ok &= (j >= 0) & (j < n_cols);
+        saa[base + 32 * (int64_t)k] = aa[lo + k];
+        sja[base + 32 * (int64_t)k] = ok ? (int32_t)j : 0;
+    }
+    if (!ok) atomicOr(bad, 1u);
+    if (len > 0 && ok) atomicMax(cmax + row / kSlice, (int32_t)ja[lo + len - 1]);
 }
 
 struct PlainSpmv {
@@ -367,6 +415,131 @@ zk_csr* build_sell(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, c
     return A;
 }
 
+
+// Host CSR -> device SELL-32 without host passes over the rows: ia goes up
+// first and the row lengths, slice widths and offsets are computed on the
+// device (CUB scan), then ja/aa stream up in chunks of ~kChunkNnz entries
+// on a copy stream through two device staging buffers while the scatter of
+// the previous chunk runs (int64 -> int32 narrowing and the column range
+// check happen in the scatter).  Returns nullptr (nothing allocated that
+// is not freed) when the matrix has rows longer than kShortMax -- their side
+// CSR is built by build_sell -- after the row pointers were verified.
+zk_csr* build_sell_streamed(zk_context* c, int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* ia_h,
+                            const int64_t* ja_h, const double2* aa_h) {
+    constexpr int64_t kChunkNnz = int64_t(1) << 25;  // 32M entries: 768 MB per staging buffer
+    cudaStream_t st = c->stream;
+    if (!c->copy_stream) {
+        ZK_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : c->up_ev) ZK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int64_t nslices = (n_rows + kSlice - 1) / kSlice;
+    int64_t* ia_d = dalloc<int64_t>(c, n_rows + 1);
+    uint8_t* rowlen = dalloc<uint8_t>(c, nslices * kSlice);
+    int64_t* swidth = dalloc<int64_t>(c, nslices + 1);
+    int64_t* slice_off = dalloc<int64_t>(c, nslices + 1);
+    unsigned long long* info = dalloc<unsigned long long>(c, 4);
+    ZK_CUDA(cudaMemsetAsync(info, 0, 4 * sizeof(unsigned long long), st));
+    ZK_CUDA(cudaMemsetAsync(rowlen, 0, nslices * kSlice, st));
+    ZK_CUDA(cudaMemsetAsync(swidth, 0, sizeof(int64_t) * (nslices + 1), st));
+    ZK_CUDA(cudaMemcpyAsync(ia_d, ia_h, sizeof(int64_t) * (n_rows + 1), cudaMemcpyHostToDevice, st));
+    k_rowinfo<<<(unsigned)((nslices * kSlice + 255) / 256), 256, 0, st>>>(n_rows, ia_d, rowlen, swidth, info);
+    ZK_CUDA(cudaGetLastError());
+    c->launches++;
+    size_t tmp_bytes = 0;
+    ZK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, swidth, slice_off, nslices + 1, st));
+    void* tmp = c->alloc.alloc(tmp_bytes ? tmp_bytes : 1);
+    ZK_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, swidth, slice_off, nslices + 1, st));
+    unsigned long long h_info[4];
+    int64_t total = 0;
+    ZK_CUDA(cudaMemcpyAsync(h_info, info, sizeof(h_info), cudaMemcpyDeviceToHost, st));
+    ZK_CUDA(cudaMemcpyAsync(&total, slice_off + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    ZK_CUDA(cudaStreamSynchronize(st));
+    c->alloc.free(tmp);
+    c->alloc.free(swidth);
+    c->alloc.free(info);
+    auto release = [&]() {
+        c->alloc.free(ia_d);
+        c->alloc.free(rowlen);
+        c->alloc.free(slice_off);
+    };
+    if (h_info[0]) {
+        release();
+        throw ZkError{ZK_ERR_FORMAT, "row pointers are not nondecreasing"};
+    }
+    if (h_info[1]) {  // long rows: the host-side builder makes their side CSR
+        release();
+        return nullptr;
+    }
+    zk_csr* A = new zk_csr();
+    std::memset(A, 0, sizeof(*A));
+    A->ctx = c;
+    A->n_rows = n_rows;
+    A->n_cols = n_cols;
+    A->nnz = nnz;
+    A->nnz_elide = nnz;
+    A->nslices = nslices;
+    A->nblocks = (n_rows + kBlock - 1) / kBlock;
+    A->wmax = (int32_t)h_info[2];
+    A->sell_elems = total;
+    A->slice_off = slice_off;
+    A->rowlen = rowlen;
+    A->aa = dalloc<double2>(c, total);
+    A->ja = dalloc<int32_t>(c, total);
+    A->slice_cmax = dalloc<int32_t>(c, nslices);
+    ZK_CUDA(cudaMemsetAsync(A->slice_cmax, 0xff, sizeof(int32_t) * (nslices ? nslices : 1), st));
+    ZK_CUDA(cudaMemsetAsync(A->aa, 0, sizeof(double2) * (total ? total : 1), st));
+    ZK_CUDA(cudaMemsetAsync(A->ja, 0, sizeof(int32_t) * (total ? total : 1), st));
+    // chunked H2D (copy stream) || scatter (compute stream), two staging buffers
+    const int64_t cap = nnz < kChunkNnz ? nnz : kChunkNnz;
+    int64_t* sja[2];
+    double2* saa[2];
+    for (int b = 0; b < 2; ++b) {
+        sja[b] = dalloc<int64_t>(c, cap);
+        saa[b] = dalloc<double2>(c, cap);
+    }
+    cudaEvent_t* ev_copy = c->up_ev;       // [0], [1]
+    cudaEvent_t* ev_free = c->up_ev + 2;   // [2], [3]
+    ZK_CUDA(cudaEventRecord(ev_free[0], st));  // staging free once the memsets above are ordered
+    ZK_CUDA(cudaEventRecord(ev_free[1], st));
+    int64_t r0 = 0, k = 0;
+    while (r0 < n_rows) {
+        // rows [r0, r1): as many as fit in one staging buffer (rows are <= 65 entries)
+        const int64_t nz0 = ia_h[r0];
+        const int64_t* lim = std::upper_bound(ia_h + r0 + 1, ia_h + n_rows + 1, nz0 + cap);
+        int64_t r1 = (int64_t)(lim - ia_h) - 1;
+        if (r1 <= r0) r1 = r0 + 1;
+        const int64_t cnt = ia_h[r1] - nz0;
+        const int b = (int)(k & 1);
+        ZK_CUDA(cudaStreamWaitEvent(c->copy_stream, ev_free[b], 0));
+        if (cnt > 0) {
+            ZK_CUDA(cudaMemcpyAsync(sja[b], ja_h + nz0, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, c->copy_stream));
+            ZK_CUDA(cudaMemcpyAsync(saa[b], aa_h + nz0, sizeof(double2) * cnt, cudaMemcpyHostToDevice, c->copy_stream));
+        }
+        ZK_CUDA(cudaEventRecord(ev_copy[b], c->copy_stream));
+        ZK_CUDA(cudaStreamWaitEvent(st, ev_copy[b], 0));
+        k_sell_scatter_chunk<<<(unsigned)((r1 - r0 + 255) / 256), 256, 0, st>>>(
+            r0, r1, n_cols, ia_d, nz0, sja[b], saa[b], slice_off, rowlen, A->aa, A->ja, A->slice_cmax, c->counter + 1);
+        ZK_CUDA(cudaGetLastError());
+        c->launches++;
+        ZK_CUDA(cudaEventRecord(ev_free[b], st));
+        r0 = r1;
+        ++k;
+    }
+    unsigned int bad = 0;
+    ZK_CUDA(cudaMemcpyAsync(&bad, c->counter + 1, sizeof(bad), cudaMemcpyDeviceToHost, st));
+    ZK_CUDA(cudaStreamSynchronize(st));
+    for (int b = 0; b < 2; ++b) {
+        c->alloc.free(sja[b]);
+        c->alloc.free(saa[b]);
+    }
+    c->alloc.free(ia_d);
+    if (bad) {
+        ZK_CUDA(cudaMemsetAsync(c->counter + 1, 0, sizeof(unsigned int), st));
+        destroy_sell(A);
+        throw ZkError{ZK_ERR_FORMAT, "column index out of range"};
+    }
+    return A;
+}
 
 void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
     if (A->n_rows == 0) return;
