@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import ctypes
 import time
+import weakref
 
 import numpy as np
 
@@ -267,7 +268,7 @@ class ShardedBiCGStab:
     """
 
     def __init__(self, bounds, rank: int, ia, ja, aa, nnz_global: int, jacobi: bool = True,
-                 max_iterations: int = 1000, group=None, transport: str = "nccl"):
+                 max_iterations: int = 1000, group=None, transport: str = "nccl", layout=None):
         self.bounds = np.asarray(bounds, dtype=np.int64)
         self.world = len(self.bounds) - 1
         self.rank = rank
@@ -278,8 +279,13 @@ class ShardedBiCGStab:
         ia = np.asarray(ia, dtype=np.int64)
         if ia.shape[0] != self.n + 1:
             raise DimensionError(f"shard has {self.n} rows but ia has {ia.shape[0]} pointers")
-        ja_local, halo = localize(ja, self.row0, self.row1)
-        self.plan = halo_plan(rank, self.bounds, halo, group)
+        # host-side shard layout (renumbered columns, halo plan): computed here,
+        # or reused from an earlier shard of the same immutable matrix
+        if layout is None:
+            ja_local, halo = localize(ja, self.row0, self.row1)
+            layout = (ja_local, halo, halo_plan(rank, self.bounds, halo, group))
+        ja_local, halo, self.plan = layout
+        self.layout = layout
         self.n_halo = int(halo.shape[0])
         self.rank_blocks = np.asarray([-(-(int(self.bounds[q + 1] - self.bounds[q])) // BLOCK)
                                        for q in range(self.world)], dtype=np.int64)
@@ -457,6 +463,9 @@ class ShardedBiCGStab:
         return x, report
 
 
+_LAYOUTS = weakref.WeakKeyDictionary()  # CsrMatrix -> {(world, rank): (bounds, layout)}
+
+
 def solve_bicgstab_sharded(A: CsrMatrix, b, M: Preconditioner | None = None, cfg: SolverConfig | None = None,
                            group=None, transport: str = "nccl"):
     """Row-sharded counterpart of :func:`krylov.solve_bicgstab` for one rank
@@ -472,12 +481,24 @@ def solve_bicgstab_sharded(A: CsrMatrix, b, M: Preconditioner | None = None, cfg
     if bvec.shape[0] != n:
         raise DimensionError(f"matrix is {n}x{n} but right-hand side has {bvec.shape[0]} elements")
     M = M if M is not None else Preconditioner.identity()
-    bounds = partition_rows(A.ia, world)
+    # the partition and the shard layout depend only on the (immutable) matrix
+    # and the group size: computed once per matrix; the device shard (upload,
+    # SELL layout, workspace) is built on every call
+    key = (world, rank)
+    cached = _LAYOUTS.get(A, {}).get(key)
+    if cached is None:
+        bounds = partition_rows(A.ia, world)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        lo, hi = int(A.ia[r0]), int(A.ia[r1])
+        ja_local, halo = localize(A.ja[lo:hi], r0, r1)
+        cached = (bounds, (ja_local, halo, halo_plan(rank, bounds, halo, group)))
+        _LAYOUTS.setdefault(A, {})[key] = cached
+    bounds, layout = cached
     r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
     lo, hi = int(A.ia[r0]), int(A.ia[r1])
     sh = ShardedBiCGStab(bounds, rank, A.ia[r0:r1 + 1] - lo, A.ja[lo:hi], A.aa[lo:hi], A.nnz,
                          jacobi=M.kind == "jacobi", max_iterations=cfg.max_iterations, group=group,
-                         transport=transport)
+                         transport=transport, layout=layout)
     guess = cfg.initial_guess
     x0 = None if guess is None else np.asarray(guess.data, dtype=np.complex128)[r0:r1]
     minv = M.data[r0:r1] if M.kind == "jacobi" else None

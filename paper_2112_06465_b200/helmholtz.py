@@ -39,16 +39,18 @@ class HelmholtzProblem:
     velocity_field: object = None
 
     def __post_init__(self):
-        if self.dim not in (1, 2, 3):
-            raise ParameterError(f"dim must be 1, 2, or 3, got {self.dim!r}")
-        if self.cells_per_axis < 3:
-            raise ParameterError(f"cells_per_axis must be at least 3, got {self.cells_per_axis!r}")
-        if not (self.domain_length > 0 and math.isfinite(self.domain_length)):
-            raise ParameterError(f"domain_length must be positive, got {self.domain_length!r}")
-        if not (self.velocity > 0 and math.isfinite(self.velocity)):
-            raise ParameterError(f"velocity must be positive, got {self.velocity!r}")
-        if not (self.frequency >= 0 and math.isfinite(self.frequency)):
-            raise ParameterError(f"frequency must be nonnegative, got {self.frequency!r}")
+        checks = (  # (condition, message) -- the reference's ParameterError texts (helmholtz.py:52-65)
+            (self.dim in (1, 2, 3), f"dim must be 1, 2, or 3, got {self.dim!r}"),
+            (self.cells_per_axis >= 3, f"cells_per_axis must be at least 3, got {self.cells_per_axis!r}"),
+            (self.domain_length > 0 and math.isfinite(self.domain_length),
+             f"domain_length must be positive, got {self.domain_length!r}"),
+            (self.velocity > 0 and math.isfinite(self.velocity), f"velocity must be positive, got {self.velocity!r}"),
+            (self.frequency >= 0 and math.isfinite(self.frequency),
+             f"frequency must be nonnegative, got {self.frequency!r}"),
+        )
+        for ok, message in checks:
+            if not ok:
+                raise ParameterError(message)
 
     @property
     def wavenumber(self) -> float:
@@ -92,34 +94,40 @@ def assemble(p: HelmholtzProblem):
     return CsrMatrix(n, n, aa, ja, ia, validate=False), ZVector(rhs)
 
 
-_CONFIG_KEYS = {"dim": int, "cells": int, "length": float, "frequency": float, "velocity": float}
+_KEY_TYPES = {"dim": int, "cells": int, "length": float, "frequency": float, "velocity": float}
 
 
-def load_problem_config(path) -> HelmholtzProblem:
-    """key=value problem file (helmholtz.py:211-249): dim, cells, length,
-    frequency, velocity; '#' comments; unit interior source."""
+def _config_values(path):
+    """key -> typed value of a key=value file ('#' comments), ParseError with line numbers."""
     values = {}
     with open(path, "r", encoding="ascii") as fh:
         for lineno, raw in enumerate(fh, start=1):
             text = raw.split("#", 1)[0].strip()
             if not text:
                 continue
-            if "=" not in text:
+            key, eq, val = text.partition("=")
+            if not eq:
                 raise ParseError(f"expected key=value, got {text!r}", line=lineno)
-            key, _, val = text.partition("=")
             key, val = key.strip().lower(), val.strip()
-            if key not in _CONFIG_KEYS:
+            convert = _KEY_TYPES.get(key)
+            if convert is None:
                 raise ParseError(f"unknown key {key!r}", line=lineno)
             try:
-                values[key] = _CONFIG_KEYS[key](val)
+                values[key] = convert(val)
             except ValueError:
                 raise ParseError(f"bad value for {key}: {val!r}", line=lineno) from None
-    for required in ("dim", "cells"):
-        if required not in values:
-            raise ParseError(f"missing required key {required!r}")
+    return values
+
+
+def load_problem_config(path) -> HelmholtzProblem:
+    """Problem file (helmholtz.py:211-249): dim and cells required; length,
+    frequency, velocity default to 1, 0, 1; unit interior source."""
+    v = _config_values(path)
+    missing = [k for k in ("dim", "cells") if k not in v]
+    if missing:
+        raise ParseError(f"missing required key {missing[0]!r}")
     try:
-        return HelmholtzProblem(dim=values["dim"], cells_per_axis=values["cells"],
-                                domain_length=values.get("length", 1.0), frequency=values.get("frequency", 0.0),
-                                velocity=values.get("velocity", 1.0), source=1 + 0j)
+        return HelmholtzProblem(dim=v["dim"], cells_per_axis=v["cells"], domain_length=v.get("length", 1.0),
+                                frequency=v.get("frequency", 0.0), velocity=v.get("velocity", 1.0), source=1 + 0j)
     except ParameterError as exc:
         raise ParseError(str(exc)) from exc
