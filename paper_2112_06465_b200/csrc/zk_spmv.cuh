@@ -98,6 +98,7 @@ struct SellView {
     // spreads over every SM; fused-reduction pipelines keep 4096-row blocks
     int32_t spb;
     int64_t nvb;
+    bool prefetch;        // L2 bulk prefetch of each slice's new x rows (one more TMA op per slice)
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
 };
@@ -1072,7 +1073,7 @@ __device__ __forceinline__ void sell_pipeline(const SellView& A, const double2* 
                         bulk_g2s(stage + A.ja_off, A.ja + off, cnt * 4u, &full[lane], pol);
                     }
                 }
-                if (c == 0 && cm_hi >= cm_lo) {  // x rows this slice is first to touch -> L2
+                if (c == 0 && cm_hi >= cm_lo && A.prefetch) {  // x rows this slice is first to touch -> L2
                     const uint32_t nb = (uint32_t)min(cm_hi - cm_lo + 1, 4096) * 16u;
                     bulk_prefetch_l2(x0 + cm_lo, nb);
                     if (x1) bulk_prefetch_l2(x1 + cm_lo, nb);
