@@ -16,9 +16,10 @@
 //
 // Kernels used per step:
 //   * SpMV phases: the persistent TMA pipeline of zk_spmv.cuh with bodies
-//     for r0 = b - A x0 (+ ||b||, ||r0||, <r0, r0>), y = A z (+ a copy),
-//     u = A z fused with <r~, u> (the BiCG pivot), and the true residual
-//     ||b - A x|| / ||b|| whose finish() does the reference's bookkeeping.
+//     for r0 = b - A x0 (+ ||b||, ||r0||, <r0, r0>) and y = A z (+ a copy);
+//     the BiCG pivot <r~, A z> and the true residual ||b - A x|| / ||b||
+//     (whose finish() does the reference's bookkeeping) are passes on the
+//     level-1 engine after a plain SpMV.
 //   * Reductions: the block-plan kernels of zk_blas1.cu with a Gate,
 //     writing their scalar into the state block (streaming ordered fold).
 //   * Elementwise: k_pairs (a batch of independent zscal+zaxpy / zaxpy
@@ -32,6 +33,7 @@
 
 #include "zk_internal.h"
 #include "zk_blockred.cuh"
+#include "zk_l1pipe.cuh"
 #include "zk_spmv.cuh"
 
 namespace zk {
@@ -150,22 +152,6 @@ struct KPlainBody {
     __device__ void finish(const double*) {}
 };
 
-// u = A z and <r~, u> in one pass (krylov.py:348-349: u[j+1] = op(u[j]),
-// pivot = zdot(r_shadow, u[j+1]))
-struct KDotBody {
-    static constexpr int kNC = 1, kNR = 0, kSV = 1;  // staged: r~
-    static constexpr int kNP = 2;
-    double2* y;
-    double2* result;
-    bool fma;
-    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[1], const double2 (&w)[1], double2 (&tc)[1],
-                                        double (&)[1]) {
-        y[r] = v[0];
-        tc[0] = f1(conjz(w[0]), v[0], fma);
-    }
-    __device__ void finish(const double* t) { *result = make_double2(t[0], t[1]); }
-};
-
 // _Run.true_relative_residual (krylov.py:183-186) and what the caller does with it:
 //   MODE 0  BiCGSTAB(l) residual probe (krylov.py:355-360): record + stop only when converged
 //   MODE 1  BiCGSTAB(l) end of cycle (krylov.py:403-407): record; stop when converged or at the cap
@@ -195,6 +181,25 @@ struct KResBody {
         else if (MODE == 1 && st->iterations >= st->maxit) kstop(st, KS_NOT_CONVERGED);
     }
 };
+
+// True residual as a pass over (b, A x) on the level-1 engine, after a plain
+// SpMV wrote A x: the same terms and order as KResBody's fused reduction.
+struct KResOp {
+    using V = double;
+    static constexpr int NIN = 2;  // b, A x
+    bool fma;
+    __device__ __forceinline__ double apply(int64_t, const double2 (&v)[2]) const {
+        return abs2_np(cadd(v[0], f1(make_double2(-1.0, 0.0), v[1], fma)));
+    }
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(kL1Threads, 1) k_kres_pass(L1View P, KResBody<MODE> fin, bool fma, Gate gate) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (gate.skip()) return;
+    KResOp op{fma};
+    l1_pipeline(P, op, fin, smem);
+}
 
 template <class Body>
 __global__ void __launch_bounds__(kRedPipeThreads, 1) k_kspmv_red(SellView A, const double2* __restrict__ x, Body body,
@@ -492,6 +497,7 @@ struct KrylovPlan {
     int64_t n = 0, hist_cap = 0;
     // vectors (device, n each)
     double2 *x = nullptr, *x0 = nullptr, *b = nullptr, *minv = nullptr, *rs = nullptr, *tmp = nullptr;
+    double2* ax = nullptr;         // A x of the true residual
     double2* r[kMaxEll + 1] = {};  // l: r[0..l]
     double2* u[kMaxEll + 1] = {};  // l: u[0..l]
     double2* acc = nullptr;
@@ -558,12 +564,10 @@ struct KLaunch {
         spmv(src, out, nullptr, g);
     }
     void op_dot(const double2* vin, double2* out, Gate g) {  // + pivot = <r~, out>
-        const double2* src = vin;
-        if (P->jacobi) {
-            jac(vin, P->tmp, g);
-            src = P->tmp;
-        }
-        spmv_red(src, KDotBody{out, &P->st->dot, fma}, P->rs, g);
+        // plain SpMV + the engine's dot: the per-element terms and the plan
+        // order are KDotBody's, and the pass costs less than a reducer warp
+        op(vin, out, g);
+        dot(P->rs, out, g);
     }
     void jac(const double2* vin, double2* out, Gate g) {
         k_jac<<<ew, kEwThreads, 0, s>>>(n, vin, P->minv, out, fma, g);
@@ -587,8 +591,18 @@ struct KLaunch {
         check();
     }
     template <int MODE>
-    void true_res(Gate g) {
-        spmv_red(P->x, KResBody<MODE>{P->st, P->hist, fma}, P->b, g);
+    void true_res(Gate g) {  // A x into ax, then the residual pass (as the BiCGStab loop does)
+        spmv(P->x, P->ax, nullptr, g);
+        const double2* in[2] = {P->b, P->ax};
+        const int8_t alias[2] = {0, 0};
+        L1View v;
+        size_t smem;
+        unsigned grid;
+        if (!l1_view(c, n, kReal, in, alias, 2, slots, nullptr, v, smem, grid))
+            throw ZkError{ZK_ERR_CUDA, "level-1 engine geometry"};
+        ZK_CUDA(cudaFuncSetAttribute(k_kres_pass<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_kres_pass<MODE><<<grid, kL1Threads, smem, s>>>(v, KResBody<MODE>{P->st, P->hist, fma}, fma, g);
+        check();
     }
     void curx(Gate g) {
         k_curx<<<ew, kEwThreads, 0, s>>>(n, P->x0, P->acc, P->jacobi ? P->minv : nullptr, P->x, fma, g);
@@ -728,8 +742,8 @@ void destroy_krylov_plan(zk_context* c, KrylovPlan* P) {
     if (!P) return;
     if (P->exec) cudaGraphExecDestroy(P->exec);
     if (P->graph) cudaGraphDestroy(P->graph);
-    void* ptrs[] = {P->x, P->x0, P->b, P->minv, P->rs, P->tmp, P->acc, P->w, P->y, P->d, P->v, P->U[0], P->U[1],
-                    P->hist, P->st, P->mr};
+    void* ptrs[] = {P->x, P->x0, P->b, P->minv, P->rs, P->tmp, P->ax, P->acc, P->w, P->y, P->d, P->v, P->U[0],
+                    P->U[1], P->hist, P->st, P->mr};
     for (void* p : ptrs)
         if (p) c->alloc.free(p);
     if (P->jacobi && P->z) c->alloc.free(P->z);
@@ -759,6 +773,7 @@ static KrylovPlan* get_kplan(zk_context* c, zk_csr* A, int32_t solver, int32_t e
     P->x0 = vec();
     P->b = vec();
     P->rs = vec();
+    P->ax = vec();
     P->minv = jacobi ? vec() : nullptr;
     P->tmp = jacobi ? vec() : nullptr;
     if (solver == KSV_BICGSTABL) {
