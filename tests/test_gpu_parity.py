@@ -277,3 +277,26 @@ def test_long_rows_warp_path_vs_oracle(swap):
     finally:
         Z.set_arithmetic(True, 262144)
         O.set_arith(True, 262144)
+
+
+def test_solver_graph_follows_arithmetic_changes():
+    """The captured solver graph carries the fingerprint in its kernel
+    parameters (FMA formula, numpy's elision swap): changing it with
+    set_arithmetic between solves must rebuild the graph, not replay stale
+    parameters."""
+    n, ia, ja, aa, b = problems.helmholtz_fd(3, 41, frequency=41 / 12.0, damping=0.3)  # 64000 rows, nnz > 16384
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    M = Z.build_jacobi(A)
+    minv = M.data
+    cfg = Z.SolverConfig(tolerance=1e-8, max_iterations=40)
+    try:
+        for fma, elide in ((True, 262144), (True, 1 << 62), (False, 262144), (True, 262144)):
+            Z.set_arithmetic(fma, elide)
+            O.set_arith(fma, elide)
+            x, rep = Z.solve_bicgstab(A, Z.ZVector(b), Z.Preconditioner("jacobi", minv), cfg)
+            xo, hist, it, st, _ = O.bicgstab(n, ia, ja, aa, b, minv, None, 1e-8, 40)
+            assert np.array(rep.residual_history).tobytes() == np.array(hist).tobytes(), (fma, elide)
+            assert bits(x.data) == bits(xo), (fma, elide)
+    finally:
+        Z.set_arithmetic(True, 262144)
+        O.set_arith(True, 262144)
