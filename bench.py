@@ -188,14 +188,13 @@ def algorithmic_bytes(n: int, nnz: int):
     return {
         "spmv": A,
         "spmv_pivot": A,                      # v = A p^ (plain pipeline)
-        "spmv2": A + 32 * n,                  # A x and v = A p^ in one matrix pass (two gathers, two writes)
         "res_pass": 32 * n,                   # ||b - A x||: b, A x
         "pivot_first": A,
         "pivot_dot": 32 * n,                  # <r~, v>: r~, v
         "pivot_first_dot": 32 * n,
         "spmv_t": A,                          # t = A s^
         "tt_ts": 32 * n,                      # <t, t>, <t, s>: t, s
-        "true_res": Ar + 32 * n,              # A, x, b
+        "true_res": A,                        # t = A x (plain pipeline; b is read by the residual pass)
         "p_next": 96 * n,                     # p, v, r, minv -> p, p^
         "true_res_s": Ar + 32 * n,
         "s_update": 80 * n,
@@ -302,11 +301,11 @@ def run_zk(args, dist: Dist):
             if name in B and name not in conditional:
                 entry["gbs"] = round(B[name] / (avg * 1e-3) / 1e9, 1)
             phases[name] = entry
-    body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "tt_ts", "xr_update", "true_res", "p_next",
-                        "spmv2", "spmv_pivot", "res_pass", "pivot_dot")
+    body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "tt_ts", "xr_update", "true_res", "res_pass",
+                        "p_next", "spmv_pivot", "pivot_dot")
             if p in phases]
-    kernel_names = {"spmv2": "k_spmv2_phase", "spmv_t": "k_spmv_phase", "spmv_pivot": "k_spmv_phase",
-                    "res_pass": "k_res_pass", "true_res": "k_true_res<1>",
+    kernel_names = {"spmv_t": "k_spmv_phase", "spmv_pivot": "k_spmv_phase", "true_res": "k_spmv_phase",
+                    "res_pass": "k_res_pass",
                     "s_update": "k_s_update_pipe", "xr_update": "k_xr_update_pipe", "tt_ts": "k_tt_ts_pass",
                     "pivot_dot": "k_pivot_pass", "p_next": "k_p_next"}
     # dominant kernel = the most device time per solve, summed over the

@@ -91,10 +91,9 @@ zk_status zk_event_elapsed(zk_context* ctx, int start_slot, int stop_slot, doubl
  * the host and brackets every phase kernel with CUDA events; zk_profile_read
  * returns the accumulated device time and launch count per phase, in this
  * order: setup, p_first, pivot_first, pivot_first_dot, s_update, x_alpha,
- * true_res_s, spmv_t, tt_ts, xr_update, true_res, p_next, spmv_pivot, spmv2
- * (A x and A p^ in one matrix pass), res_pass, pivot_dot.  Phases the loop
- * shape does not use report 0 launches. */
-#define ZK_NPHASES 16
+ * true_res_s, spmv_t, tt_ts, xr_update, true_res (A x), res_pass, p_next,
+ * spmv_pivot, pivot_dot. */
+#define ZK_NPHASES 15
 zk_status zk_profile_enable(zk_context* ctx, int on);
 zk_status zk_profile_read(zk_context* ctx, double* total_ms, int64_t* launches);
 

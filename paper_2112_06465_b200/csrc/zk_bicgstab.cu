@@ -334,35 +334,6 @@ __global__ void __launch_bounds__(kRedPipeThreads, 1) k_true_res(SellView A, Sol
     sell_run<1>(A, B.x, nullptr, body, R, smem);
 }
 
-// ---- K61 + next K2 in ONE matrix pass: t = A x and v = A p^ ------------------
-// (krylov.py:291 true residual, :267 next pivot product).  Kp runs first, so
-// both gathered vectors are final; the residual's reduction pass then runs
-// before the pivot's, keeping the reference's order of checks (record/stop,
-// then the next pivot).  t is free here (K5 consumed it; the next K4
-// rewrites it).  One stream of the 4.3 GB matrix serves both products.
-struct PhaseSpmv2Body {
-    static constexpr int kNC = 0, kNR = 0, kSV = 0;
-    double2* __restrict__ y0;
-    double2* __restrict__ y1;
-    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[2], const double2 (&)[1], double2 (&)[1],
-                                        double (&)[1]) {
-        y0[r] = v[0];
-        y1[r] = v[1];
-    }
-    __device__ __forceinline__ void finish(const double*) {}
-};
-
-__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv2_phase(SellView A, const double2* __restrict__ x0,
-                                                                 const double2* __restrict__ x1,
-                                                                 double2* __restrict__ y0, double2* __restrict__ y1,
-                                                                 const SolverState* st) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    if (st->done) return;
-    PhaseSpmv2Body body{y0, y1};
-    const RedCfg R{};
-    sell_run<2>(A, x0, x1, body, R, smem);
-}
-
 // true residual pass: ||b + F1(-1, A x)||^2 over (b, A x) -> record / stop
 struct ResOp {
     using V = double;
@@ -539,10 +510,8 @@ struct Launch {
     L1View l1s, l1x, l1p, l1t;
     size_t smem_l1s = 0, smem_l1x = 0, smem_l1p = 0, smem_l1t = 0;
     unsigned grid_l1s = 0, grid_l1x = 0, grid_l1p = 0, grid_l1t = 0;
-    SellView Apl, Apl2;       // plain SpMV phases (K4, first K2; K61 + K2 with two vectors)
-    size_t smem_pl = 0, smem_pl2 = 0;
-    bool fuse2 = false;       // one matrix pass for K61 + K2 (consumer-bound: experiments only)
-    bool respass = false;     // K61 as plain SpMV + residual pass instead of the reducer-warp SpMV
+    SellView Apl;             // plain SpMV phases (K2, K4, K61 products)
+    size_t smem_pl = 0;
     L1View l1r;               // true-residual pass
     size_t smem_l1r = 0;
     unsigned grid_l1r = 0;
@@ -554,7 +523,7 @@ struct Launch {
 enum Phase : int {
     PH_SETUP, PH_P_FIRST, PH_PIVOT_FIRST, PH_PIVOT_FIRST_DOT,          // prologue
     PH_S_UPDATE, PH_X_ALPHA, PH_TRUE_RES_S, PH_SPMV_T, PH_TT_TS, PH_XR_UPDATE,
-    PH_TRUE_RES, PH_P_NEXT, PH_SPMV_PIVOT, PH_SPMV2, PH_RES_PASS, PH_PIVOT_DOT,
+    PH_TRUE_RES, PH_RES_PASS, PH_P_NEXT, PH_SPMV_PIVOT, PH_PIVOT_DOT,
     PH_COUNT
 };
 
@@ -596,10 +565,12 @@ void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr)
 }
 constexpr int kPrologueKernels = 4;
 
-// One iteration: K3, [K3x, K6x], K4 (SpMV + pass), K5; then either K61
-// (residual reduction fused into its SpMV), Kp, the next K2's SpMV -- or,
-// with L.fuse2, Kp and ONE matrix pass for K61's A x and the next K2's A p^
-// followed by the residual pass (record / stop); and the pivot pass.
+// One iteration: K3, [K3x, K6x], K4 (SpMV + pass), K5, K61 (A x into t +
+// the residual pass: record / stop), Kp, K2 (SpMV + pivot pass; sets the
+// WHILE condition).  K61 is a plain SpMV + pass like K2/K4 (786 vs 794 us for
+// the reducer-warp SpMV on C4); one matrix pass for K61's A x and K2's A p^
+// measured slower (1703 vs 799 + 716 us: two gathered vectors make the
+// consumers the bottleneck).
 void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle cond, int use_cond,
                  PhaseEvents* pe = nullptr) {
     SolverBufs B = L.P->bufs;
@@ -609,31 +580,17 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     { PhaseScope ps(pe, PH_SPMV_T); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st); }
     { PhaseScope ps(pe, PH_TT_TS); k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t); }
     { PhaseScope ps(pe, PH_XR_UPDATE); k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); }
-    if (L.fuse2) {
-        { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
-        {
-            PhaseScope ps(pe, PH_SPMV2);
-            k_spmv2_phase<<<L.ppg, kPipeThreads, L.smem_pl2, s>>>(L.Apl2, B.x, B.ph, B.t, B.v, B.st);
-        }
-        { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
-    } else {
-        if (L.respass) {  // K61 as a plain SpMV into t + the residual pass
-            { PhaseScope ps(pe, PH_TRUE_RES); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st); }
-            { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
-        } else {
-            PhaseScope ps(pe, PH_TRUE_RES);
-            k_true_res<1><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red);
-        }
-        { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
-        { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
-    }
+    { PhaseScope ps(pe, PH_TRUE_RES); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st); }
+    { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
+    { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
+    { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
     {
         PhaseScope ps(pe, PH_PIVOT_DOT);
         k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
     }
 }
 // launches per loop trip
-inline int body_kernels(const Launch& L) { return (!L.fuse2 && L.respass) ? 11 : 10; }
+inline int body_kernels(const Launch&) { return 11; }
 
 void accumulate(zk_context* c, PhaseEvents& pe) {
     for (int k = 0; k < PH_COUNT; ++k) {
@@ -650,12 +607,10 @@ void accumulate(zk_context* c, PhaseEvents& pe) {
 void set_attrs(const Launch& L) {
     smem_attr(k_setup, L.smem_s);
     smem_attr(k_spmv_phase, L.smem_pl);
-    smem_attr(k_spmv2_phase, L.smem_pl2);
     smem_attr(k_res_pass, L.smem_l1r);
     smem_attr(k_pivot_pass, L.smem_l1p);
     smem_attr(k_tt_ts_pass, L.smem_l1t);
     smem_attr(k_true_res<0>, L.smem_r);
-    smem_attr(k_true_res<1>, L.smem_r);
     smem_attr(k_s_update_pipe, L.smem_l1s);
     smem_attr(k_xr_update_pipe, L.smem_l1x);
 }
@@ -761,22 +716,9 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.Ar = sell_view(A, c, ex_r, 1);
     L.Ar.sv[0] = B.b;
     L.Apl = sell_view(A, c, 0, 0);
-    L.Apl2 = sell_view(A, c, 0, 0);
     L.ppg = plain_grid(A, L.Apl);
-    plain_grid(A, L.Apl2);
-    {
-        // one matrix pass for K61 + K2 measured slower on C4 (1703 us vs 799 +
-        // 716 us: two gathered vectors make the consumers the bottleneck);
-        // ZK_FUSE2=1 selects it for experiments
-        const char* e = std::getenv("ZK_FUSE2");
-        L.fuse2 = e && e[0] == '1';
-        // K61 as plain SpMV + residual pass: 786 vs 794 us on C4 (profiles/r02)
-        const char* r = std::getenv("ZK_RESPASS");
-        L.respass = !(r && r[0] == '0');
-    }
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_pl = pipe_smem_bytes(L.Apl, 0);
-    L.smem_pl2 = pipe_smem_bytes(L.Apl2, 0);
     L.smem_r = pipe_smem_bytes(L.Ar, ex_r);
     L.pc = c->plans_for(n, kBlock, kComplex);
     L.pr = c->plans_for(n, kBlock, kReal);
