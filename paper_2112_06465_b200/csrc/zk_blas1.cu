@@ -4,6 +4,7 @@
 // (16-byte, coalesced) with 4 independent elements per thread in flight.
 // Reductions run one CTA per ReductionPlan block (numpy's pairwise order,
 // zk_blockred.cuh) and a one-warp kernel folds the block partials in order.
+#include <cstdlib>
 #include <cstring>
 
 #include "zk_internal.h"
@@ -260,14 +261,23 @@ double* fold_slots(zk_context* c, int64_t count) {
 // staged inputs; false when the plans do not fit the engine (tail block with
 // more stages than a full one), so the caller takes the block-per-CTA path.
 bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
-             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid, int vbytes) {
+             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid, int vbytes, int fine) {
     if (n <= 0) return false;
     const PlanPtrs p = c->plans_for(n, kBlock, kind);
     const PlanHeader* hf = reinterpret_cast<const PlanHeader*>(c->plan_host(kBlock - 1, kind));
     const int64_t nb = (n + kBlock - 1) / kBlock;
     const int32_t tail_len = (int32_t)(n - (nb - 1) * kBlock) - 1;
     const PlanHeader* ht = reinterpret_cast<const PlanHeader*>(c->plan_host(tail_len, kind));
-    if (ht->nstages > hf->nstages) return false;
+    int staged_inputs = 0;
+    for (int v = 0; v < nin_op; ++v) staged_inputs += in[v] != nullptr;
+    if (fine < 0) {
+        // finer stages (half-size ring slots, twice as many in flight) for ops
+        // that stage many vectors; ZK_L1FINE = 0 / 1 / 2: never / default / always
+        const char* e = std::getenv("ZK_L1FINE");
+        const int mode = e ? std::atoi(e) : 1;
+        fine = mode == 2 ? 1 : (mode == 0 ? 0 : (staged_inputs >= 4 ? 1 : 0));
+    }
+    if (ht->nstages[fine] > hf->nstages[fine]) return false;
     std::memset(&P, 0, sizeof(P));
     P.n = n;
     P.nblocks = nb;
@@ -279,7 +289,9 @@ bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, c
         if (in[v]) ++staged;
     }
     P.nin = staged;
-    P.slot_bytes = staged * kStageMaxElems * 16;
+    P.fine = fine;
+    P.smax = fine ? kStageMaxElemsFine : kStageMaxElems;
+    P.slot_bytes = staged * P.smax * 16;
     const size_t head = l1_head_bytes(vbytes ? vbytes : (kind == kComplex ? 16 : 8));
     const size_t limit = 227 * 1024 - kL1StaticSmem;
     int ns = (int)((limit - head) / (size_t)P.slot_bytes);

@@ -51,7 +51,9 @@ struct L1View {
     int8_t alias[kL1MaxIn];       // for a null in[v]: the input whose staged copy it reads (same vector)
     int32_t nin;                  // staged (non-null) inputs
     int32_t ns;                   // ring slots
-    int32_t slot_bytes;           // nin * kStageMaxElems * 16
+    int32_t slot_bytes;           // nin * smax * 16
+    int32_t fine;                 // stage table: 0 (<= 32 items) or 1 (<= 16 items, half-size slots)
+    int32_t smax;                 // elements per staged vector in a slot (kStageMaxElems[Fine])
     double* slots;                // streaming fold slots (nblocks * NP), or nullptr
     double* partials;             // stored partials (nblocks * NP) when slots == nullptr
 };
@@ -61,7 +63,8 @@ struct L1View {
 // reduction terms of vbytes (0: 16 complex / 8 real).  False when it does
 // not fit the engine.
 bool l1_view(zk_context* c, int64_t n, int32_t kind, const double2* const* in, const int8_t* alias, int nin_op,
-             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid, int vbytes = 0);
+             double* slots, double* partials, L1View& P, size_t& smem, unsigned& grid, int vbytes = 0,
+             int fine = -1);
 
 template <typename V>
 struct L1Smem {
@@ -86,7 +89,7 @@ inline size_t l1_head_bytes(int vbytes) {
 // Copies a plan blob (header..stage table) into shared memory; whole warp.
 __device__ __forceinline__ const char* l1_cache_plan(const char* g, char* s) {
     const PlanHeader* h = reinterpret_cast<const PlanHeader*>(g);
-    const int bytes = h->stages_off + 16 * h->nstages;
+    const int bytes = h->stages_off[1] + 16 * h->nstages[1];
     if (bytes > L1Smem<double>::kPlanBytes) return g;
     const int4* src = reinterpret_cast<const int4*>(g);
     int4* dst = reinterpret_cast<int4*>(s);
@@ -139,15 +142,16 @@ __device__ __forceinline__ void l1_pipeline(const L1View& P, const Op& op, Fin& 
     const int ns = P.ns;
 
     const PlanHeader* hf = plan_hdr(P.plans.full);
-    const int nst_full = hf->nstages;
+    const int fine = P.fine;
+    const int nst_full = hf->nstages[fine];
     const int64_t tail_blk = P.nblocks - 1;
     const bool has_tail = P.plans.tail != P.plans.full;
     // CTA-local block k -> global block blockIdx.x + k * gridDim.x
     const int64_t nblk_cta = (P.nblocks - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const bool own_tail = has_tail && ((tail_blk - blockIdx.x) % gridDim.x == 0);
     const int64_t total_stages =
-        own_tail ? (nblk_cta - 1) * nst_full + plan_hdr(P.plans.tail)->nstages : nblk_cta * nst_full;
-    const int nst_tail_blk = own_tail ? plan_hdr(P.plans.tail)->nstages : nst_full;
+        own_tail ? (nblk_cta - 1) * nst_full + plan_hdr(P.plans.tail)->nstages[fine] : nblk_cta * nst_full;
+    const int nst_tail_blk = own_tail ? plan_hdr(P.plans.tail)->nstages[fine] : nst_full;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < ns; ++i) {
@@ -166,11 +170,11 @@ __device__ __forceinline__ void l1_pipeline(const L1View& P, const Op& op, Fin& 
         if (has_tail) l1_cache_plan(P.plans.tail, pl_tail);
     }
     __syncthreads();
-    const char* cfull = (hf->stages_off + 16 * hf->nstages <= SM::kPlanBytes) ? pl_full : P.plans.full;
+    const char* cfull = (hf->stages_off[1] + 16 * hf->nstages[1] <= SM::kPlanBytes) ? pl_full : P.plans.full;
     const char* ctail = P.plans.full;
     if (has_tail) {
         const PlanHeader* ht = plan_hdr(P.plans.tail);
-        ctail = (ht->stages_off + 16 * ht->nstages <= SM::kPlanBytes) ? pl_tail : P.plans.tail;
+        ctail = (ht->stages_off[1] + 16 * ht->nstages[1] <= SM::kPlanBytes) ? pl_tail : P.plans.tail;
     } else {
         ctail = cfull;
     }
@@ -194,7 +198,7 @@ __device__ __forceinline__ void l1_pipeline(const L1View& P, const Op& op, Fin& 
                 const char* plan;
                 int s;
                 locate(q, k, blk, plan, s);
-                const int4 st = reinterpret_cast<const int4*>(plan + plan_hdr(plan)->stages_off)[s];
+                const int4 st = reinterpret_cast<const int4*>(plan + plan_hdr(plan)->stages_off[fine])[s];
                 const int64_t e0 = blk * kBlock + st.x;
                 const uint32_t bytes = (uint32_t)(st.y - st.x) * 16u;
                 tag[lane] = (uint32_t)q;
@@ -204,7 +208,7 @@ __device__ __forceinline__ void l1_pipeline(const L1View& P, const Op& op, Fin& 
 #pragma unroll
                 for (int v = 0; v < NIN; ++v) {
                     if (P.in[v]) {
-                        bulk_g2s(dst + (size_t)slot_in * kStageMaxElems * 16, P.in[v] + e0, bytes, &full[lane], pol);
+                        bulk_g2s(dst + (size_t)slot_in * P.smax * 16, P.in[v] + e0, bytes, &full[lane], pol);
                         ++slot_in;
                     }
                 }
@@ -232,7 +236,7 @@ __device__ __forceinline__ void l1_pipeline(const L1View& P, const Op& op, Fin& 
             int s;
             locate(q, k, blk, plan, s);
             const PlanHeader* h = plan_hdr(plan);
-            const int4 st = reinterpret_cast<const int4*>(plan + h->stages_off)[s];
+            const int4 st = reinterpret_cast<const int4*>(plan + h->stages_off[fine])[s];
             const int slot = (int)(q % ns);
             while (tag[slot] != (uint32_t)q) {
             }
@@ -245,7 +249,7 @@ __device__ __forceinline__ void l1_pipeline(const L1View& P, const Op& op, Fin& 
             auto elem = [&](int be, double2 (&vals)[NIN]) {  // block element be (staged)
                 const int li = be - st.x;
 #pragma unroll
-                for (int v = 0; v < NIN; ++v) vals[v] = sbase[pos[v] * kStageMaxElems + li];
+                for (int v = 0; v < NIN; ++v) vals[v] = sbase[pos[v] * P.smax + li];
             };
             if (s == 0 && lane == 0) {  // reduceat head v[0]
                 double2 vals[NIN];

@@ -93,10 +93,10 @@ size_t build_plan(int32_t L, int32_t kind, void* out) {
         while (k < nleaves && 1 + B.leaf_start[k] + B.leaf_len[k] <= 32 * j) ++k;
         h.leaf_upto[j] = (int16_t)k;
     }
-    // stages: subtrees of the same recursion with <= kStageItems / lanes leaves
-    std::vector<int32_t> stages;  // (b_lo, b_hi, l_lo, l_hi)
-    {
-        const int32_t maxl = kStageItems / B.lanes;
+    // stages: subtrees of the same recursion with <= items / lanes leaves
+    auto make_stages = [&](int32_t items) {
+        std::vector<int32_t> stages;  // (b_lo, b_hi, l_lo, l_hi)
+        const int32_t maxl = std::max<int32_t>(1, items / B.lanes);
         auto first_leaf = [&](int32_t pos) {  // first leaf starting at or after pos
             return (int32_t)(std::lower_bound(B.leaf_start.begin(), B.leaf_start.end(), pos) - B.leaf_start.begin());
         };
@@ -129,15 +129,20 @@ size_t build_plan(int32_t L, int32_t kind, void* out) {
                 stages.insert(stages.end(), {k == 0 ? 0 : 1 + s0, 1 + s0 + l0, first_leaf(s0), first_leaf(s0 + l0)});
             }
         }
-    }
-    h.nstages = (int32_t)(stages.size() / 4);
+        return stages;
+    };
+    const std::vector<int32_t> stages = make_stages(kStageItems), stages16 = make_stages(kStageItems / 2);
+    h.nstages[0] = (int32_t)(stages.size() / 4);
+    h.nstages[1] = (int32_t)(stages16.size() / 4);
     size_t leaves_bytes = sizeof(int32_t) * 2 * (size_t)nleaves;
     size_t ops_bytes = sizeof(int32_t) * 4 * (size_t)cnt;
     size_t stages_bytes = sizeof(int32_t) * stages.size();
+    size_t stages16_bytes = sizeof(int32_t) * stages16.size();
     h.leaves_off = (int32_t)((sizeof(PlanHeader) + 15) / 16 * 16);
     h.ops_off = (int32_t)((h.leaves_off + leaves_bytes + 15) / 16 * 16);
-    h.stages_off = (int32_t)((h.ops_off + ops_bytes + 15) / 16 * 16);
-    size_t total = (h.stages_off + stages_bytes + 15) / 16 * 16;
+    h.stages_off[0] = (int32_t)((h.ops_off + ops_bytes + 15) / 16 * 16);
+    h.stages_off[1] = (int32_t)((h.stages_off[0] + stages_bytes + 15) / 16 * 16);
+    size_t total = (h.stages_off[1] + stages16_bytes + 15) / 16 * 16;
     if (out) {
         char* o = static_cast<char*>(out);
         std::memset(o, 0, total);
@@ -148,7 +153,8 @@ size_t build_plan(int32_t L, int32_t kind, void* out) {
             lv[2 * i + 1] = B.leaf_len[i];
         }
         if (cnt) std::memcpy(o + h.ops_off, ops.data(), ops_bytes);
-        std::memcpy(o + h.stages_off, stages.data(), stages_bytes);
+        std::memcpy(o + h.stages_off[0], stages.data(), stages_bytes);
+        std::memcpy(o + h.stages_off[1], stages16.data(), stages16_bytes);
     }
     return total;
 }

@@ -39,8 +39,10 @@ struct PlanHeader {
     // stage s holding block elements [b_lo, b_hi) (stage 0 also element 0,
     // the reduceat head) and leaves [l_lo, l_hi).  The TMA-fed level-1
     // engine (zk_l1pipe.cuh) streams a block stage by stage.
-    int32_t nstages;
-    int32_t stages_off;
+    // [0]: stages of <= kStageItems items; [1]: <= kStageItems / 2 (finer
+    // stages for ops that stage many vectors: more ring slots in flight)
+    int32_t nstages[2];
+    int32_t stages_off[2];
     // leaf_upto[j]: number of leaves whose elements all lie in rows [0, 32*j)
     // of the 4096-row block (element e of the segment is block row 1+e); lets
     // the SpMV kernels reduce leaves as soon as the rows under them are done.
@@ -49,6 +51,7 @@ struct PlanHeader {
 
 constexpr int kStageItems = 32;     // (leaf, lane) items per stage: one warp
 constexpr int kStageMaxElems = 520; // >= 1 + 8 * 64 (complex) and 1 + 4 * 128 (real)
+constexpr int kStageMaxElemsFine = 264;  // >= 1 + 4 * 64 and 1 + 2 * 128
 
 // Builds the plan for segment length L into `out` (host memory); returns the
 // number of bytes used.  `out` may be null to query the size.
