@@ -304,7 +304,10 @@ def run_zk(args, dist: Dist):
     body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "tt_ts", "xr_update", "true_res", "res_pass",
                         "p_next", "spmv_pivot", "pivot_dot")
             if p in phases]
-    kernel_names = {"spmv_t": "k_spmv_phase", "spmv_pivot": "k_spmv_phase", "true_res": "k_spmv_phase",
+    # matrices at most 8 entries wide (no long rows) run the narrow SpMV kernels (zk_spmv.cuh)
+    spmv_k = "k_spmv_phase_narrow" if int(np.diff(ia).max()) <= 8 and os.environ.get("ZK_NARROW") != "0" \
+        else "k_spmv_phase"
+    kernel_names = {"spmv_t": spmv_k, "spmv_pivot": spmv_k, "true_res": spmv_k,
                     "res_pass": "k_res_pass",
                     "s_update": "k_s_update_pipe", "xr_update": "k_xr_update_pipe", "tt_ts": "k_tt_ts_pass",
                     "pivot_dot": "k_pivot_pass", "p_next": "k_p_next"}

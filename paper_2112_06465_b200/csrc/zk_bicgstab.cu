@@ -213,6 +213,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_phase(SellView A, cons
     sell_run<1>(A, x, nullptr, body, R, smem);
 }
 
+__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW_MINB) k_spmv_phase_narrow(SellView A, const double2* __restrict__ x,
+                                                                          double2* __restrict__ y,
+                                                                          const SolverState* st) {
+    if (st->done) return;
+    PhaseSpmvBody body{y};
+    extern __shared__ __align__(128) unsigned char smem[];
+    narrow_dispatch(A, x, body, smem);
+}
+
 // ---- K2 pass: <r~, v> -> pivot, alpha (krylov.py:268-271) ----
 // Last kernel of the loop body: sets the graph's WHILE condition (the
 // prologue instance, use_cond = 0, runs the first iteration's K2).
@@ -556,11 +565,17 @@ struct PhaseScope {
     }
 };
 
+// A plain SpMV phase: the direct kernel for narrow matrices, else the ring.
+inline void spmv_phase(const Launch& L, cudaStream_t s, const double2* x, double2* y, const SolverState* st) {
+    if (L.Apl.narrow) k_spmv_phase_narrow<<<narrow_grid(L.Apl), kNarrowThreads, narrow_smem(L.Apl), s>>>(L.Apl, x, y, st);
+    else k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, x, y, st);
+}
+
 void launch_prologue(const Launch& L, cudaStream_t s, PhaseEvents* pe = nullptr) {
     SolverBufs B = L.P->bufs;
     { PhaseScope ps(pe, PH_SETUP); k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); }
     { PhaseScope ps(pe, PH_P_FIRST); k_p_first<<<L.ew, 256, 0, s>>>(B); }
-    { PhaseScope ps(pe, PH_PIVOT_FIRST); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
+    { PhaseScope ps(pe, PH_PIVOT_FIRST); spmv_phase(L, s, B.ph, B.v, B.st); }
     { PhaseScope ps(pe, PH_PIVOT_FIRST_DOT); k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0); }
 }
 constexpr int kPrologueKernels = 4;
@@ -577,13 +592,13 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     { PhaseScope ps(pe, PH_S_UPDATE); k_s_update_pipe<<<L.grid_l1s, kL1Threads, L.smem_l1s, s>>>(B, L.l1s); }
     { PhaseScope ps(pe, PH_X_ALPHA); k_x_alpha<<<L.ew, 256, 0, s>>>(B); }
     { PhaseScope ps(pe, PH_TRUE_RES_S); k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); }
-    { PhaseScope ps(pe, PH_SPMV_T); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st); }
+    { PhaseScope ps(pe, PH_SPMV_T); spmv_phase(L, s, B.sh, B.t, B.st); }
     { PhaseScope ps(pe, PH_TT_TS); k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t); }
     { PhaseScope ps(pe, PH_XR_UPDATE); k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); }
-    { PhaseScope ps(pe, PH_TRUE_RES); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st); }
+    { PhaseScope ps(pe, PH_TRUE_RES); spmv_phase(L, s, B.x, B.t, B.st); }
     { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
     { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
-    { PhaseScope ps(pe, PH_SPMV_PIVOT); k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st); }
+    { PhaseScope ps(pe, PH_SPMV_PIVOT); spmv_phase(L, s, B.ph, B.v, B.st); }
     {
         PhaseScope ps(pe, PH_PIVOT_DOT);
         k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
@@ -607,6 +622,7 @@ void accumulate(zk_context* c, PhaseEvents& pe) {
 void set_attrs(const Launch& L) {
     smem_attr(k_setup, L.smem_s);
     smem_attr(k_spmv_phase, L.smem_pl);
+    smem_attr(k_spmv_phase_narrow, kNarrowSmem);
     smem_attr(k_res_pass, L.smem_l1r);
     smem_attr(k_pivot_pass, L.smem_l1p);
     smem_attr(k_tt_ts_pass, L.smem_l1t);
@@ -952,7 +968,7 @@ void dist_phase(DistSolver* D, int phase) {
         case ZK_DPHASE_SETUP: k_setup<<<L.pg, kRedPipeThreads, L.smem_s, s>>>(L.As, B, L.red); break;
         case ZK_DPHASE_P_FIRST: k_p_first<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_PIVOT:
-            k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.ph, B.v, B.st);
+            spmv_phase(L, s, B.ph, B.v, B.st);
             ZK_CUDA(cudaGetLastError());
             D->c->launches++;
             k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, 0, 0);
@@ -961,14 +977,14 @@ void dist_phase(DistSolver* D, int phase) {
         case ZK_DPHASE_X_ALPHA: k_x_alpha<<<L.ew, 256, 0, s>>>(B); break;
         case ZK_DPHASE_TRUE_RES_S: k_true_res<0><<<L.pg, kRedPipeThreads, L.smem_r, s>>>(L.Ar, B, L.red); break;
         case ZK_DPHASE_SPMV_T:
-            k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.sh, B.t, B.st);
+            spmv_phase(L, s, B.sh, B.t, B.st);
             ZK_CUDA(cudaGetLastError());
             D->c->launches++;
             k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t);
             break;
         case ZK_DPHASE_XR_UPDATE: k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); break;
         case ZK_DPHASE_TRUE_RES:  // A x into t, residual pass -> slot 1
-            k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.t, B.st);
+            spmv_phase(L, s, B.x, B.t, B.st);
             ZK_CUDA(cudaGetLastError());
             D->c->launches++;
             k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r);

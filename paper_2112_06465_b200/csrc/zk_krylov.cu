@@ -217,6 +217,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_kspmv(SellView A, const dou
     sell_run<1>(A, x, nullptr, body, R, smem);
 }
 
+__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW_MINB) k_kspmv_narrow(SellView A, const double2* __restrict__ x,
+                                                                     KPlainBody body, Gate gate) {
+    if (gate.skip()) return;
+    extern __shared__ __align__(128) unsigned char smem[];
+    narrow_dispatch(A, x, body, smem);
+}
+
 // ---- elementwise kernels -------------------------------------------------------
 
 constexpr int kEwThreads = 256;
@@ -549,6 +556,12 @@ struct KLaunch {
     void spmv(const double2* x, double2* y, double2* y2, Gate g) {
         SellView v = sell_view(A, c, 0, 0);
         const unsigned grid = plain_grid(A, v);
+        if (v.narrow) {
+            ZK_CUDA(cudaFuncSetAttribute(k_kspmv_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, kNarrowSmem));
+            k_kspmv_narrow<<<narrow_grid(v), kNarrowThreads, narrow_smem(v), s>>>(v, x, KPlainBody{y, y2}, g);
+            check();
+            return;
+        }
         const size_t smem = pipe_smem_bytes(v, 0);
         ZK_CUDA(cudaFuncSetAttribute(k_kspmv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_kspmv<<<grid, kPipeThreads, smem, s>>>(v, x, KPlainBody{y, y2}, g);

@@ -101,6 +101,8 @@ struct SellView {
     bool prefetch;        // L2 bulk prefetch of each slice's new x rows (one more TMA op per slice)
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
+    bool narrow;          // plain launches: direct kernel (narrow_run) instead of the ring
+    bool narrow_tma;      // ... its per-warp TMA double-buffered variant (narrow_tma_run)
 };
 
 __device__ __forceinline__ double2 spmv_prod(const SellView& A, double2 a, double2 xv) {
@@ -588,6 +590,166 @@ __device__ __forceinline__ RowVals<NX> row_fast_dispatch(int W, const double2* _
         default: return row_fast<36, SWAP, NX>(x0, x1, saa, sja, lane, len);
     }
 }
+
+// ---- narrow matrices: one thread per row, 16 warps per SM ----------------
+// Every slice at most kNarrowMax wide and no long rows (C1/C5's 7-point
+// rows).  With 7-entry rows the ring's consumers (7 warps per SM) have too
+// few gathers in flight (C5 SpMV 648 us, 0.68 of HBM).  Default: the per-warp
+// TMA variant (narrow_tma_run, C5 421 us); narrow_run (direct loads, one warp
+// per slice, no prefetch: 509 us at 24 warps per SM) stays as ZK_NARROW=1 for
+// A/B.  Both sum in numpy's order (RowSum, the fast path's order).
+constexpr int kNarrowMax = 8;
+constexpr int kNarrowThreads = 256;
+#ifndef ZK_NARROW_MINB
+#define ZK_NARROW_MINB 2  // resident CTAs per SM (108 registers, no spills; 3 CTAs spill at 80)
+#endif
+#ifndef ZK_NARROW_LD
+#define ZK_NARROW_LD __ldcs
+#endif
+
+template <class Body>
+__device__ __forceinline__ void narrow_run(const SellView& A, const double2* __restrict__ x, Body& body) {
+    static_assert(Body::kSV == 0 && Body::kNC == 0 && Body::kNR == 0, "plain bodies only");
+    const int lane = threadIdx.x & 31;
+    const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (s >= A.nslices) return;
+    const int64_t off = A.slice_off[s];
+    const int W = (int)((A.slice_off[s + 1] - off) / kSlice);
+    const int64_t row = s * kSlice + lane;
+    const bool mine = row < A.n_rows;
+    const int len = mine ? (int)A.rowlen[row] : 0;
+    const int32_t* sja = A.ja + off + lane;
+    const double2* saa = A.aa + off + lane;
+    int32_t j[kNarrowMax];
+    double2 a[kNarrowMax], xs[kNarrowMax];
+    const double2 z = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < kNarrowMax; ++k) j[k] = k < W ? ZK_NARROW_LD(sja + 32 * k) : 0;
+#pragma unroll
+    for (int k = 0; k < kNarrowMax; ++k) a[k] = k < W ? ZK_NARROW_LD(saa + 32 * k) : z;
+#pragma unroll
+    for (int k = 0; k < kNarrowMax; ++k) xs[k] = k < len ? __ldg(x + j[k]) : z;
+    RowSum acc;
+    acc.init(len);
+#pragma unroll
+    for (int k = 0; k < kNarrowMax; ++k) acc.add(k, spmv_prod(A, a[k], xs[k]));
+    if (mine) {
+        double2 v[1] = {acc.result()}, sv[1], tc[1];
+        double tr[1];
+        body.row(row, v, sv, tc, tr);
+    }
+}
+
+// Per-warp TMA variant: a persistent warp walks slices s, s + nw, ...; the
+// next slice's values arrive by one bulk copy into the warp's other stage
+// and its columns and row lengths by loads into registers while the current
+// slice's gathers are in flight, so only the gathers' latency is exposed.
+constexpr int kNarrowWarps = kNarrowThreads / 32;
+constexpr int kNarrowStage = kNarrowMax * kSlice * 16;  // values of one slice
+constexpr int kNarrowSmem = 128 + kNarrowWarps * 2 * kNarrowStage;
+
+template <class Body>
+__device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2* __restrict__ x, Body& body,
+                                               unsigned char* smem) {
+    static_assert(Body::kSV == 0 && Body::kNC == 0 && Body::kNR == 0, "plain bodies only");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
+    unsigned char* buf = smem + 128 + (size_t)warp * 2 * kNarrowStage;
+    const int64_t ns = A.nslices, nw = (int64_t)gridDim.x * kNarrowWarps;
+    int64_t s = (int64_t)blockIdx.x * kNarrowWarps + warp;
+    if (s >= ns) return;
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncwarp();
+    const uint64_t pol = l2_evict_first_policy();
+    const double2 z = make_double2(0.0, 0.0);
+    // offsets of the current and the next slice
+    int64_t o0 = A.slice_off[s], e0 = A.slice_off[s + 1];
+    int64_t s1 = s + nw;
+    int64_t o1 = s1 < ns ? A.slice_off[s1] : 0, e1 = s1 < ns ? A.slice_off[s1 + 1] : 0;
+    if (lane == 0) {
+        mbar_arrive_expect_tx(&bar[0], (uint32_t)(e0 - o0) * 16u);
+        if (e0 > o0) bulk_g2s(buf, A.aa + o0, (uint32_t)(e0 - o0) * 16u, &bar[0], pol);
+    }
+    int32_t jc[kNarrowMax];
+    int lc;
+    {
+        const int W = (int)((e0 - o0) / kSlice);
+#pragma unroll
+        for (int q = 0; q < kNarrowMax; ++q) jc[q] = q < W ? __ldcs(A.ja + o0 + 32 * q + lane) : 0;
+        lc = s * kSlice + lane < A.n_rows ? (int)A.rowlen[s * kSlice + lane] : 0;
+    }
+    for (uint32_t k = 0; s < ns; s = s1, s1 += nw, ++k) {
+        const int st = (int)(k & 1);
+        double2 xs[kNarrowMax];
+#pragma unroll
+        for (int q = 0; q < kNarrowMax; ++q) xs[q] = q < lc ? __ldg(x + jc[q]) : z;
+        // the next slice: values by TMA into the other stage, columns and
+        // lengths into registers; offsets of the one after
+        const int64_t s2 = s1 + nw;
+        const int64_t o2 = s2 < ns ? A.slice_off[s2] : 0, e2 = s2 < ns ? A.slice_off[s2 + 1] : 0;
+        int32_t jn[kNarrowMax];
+        int ln = 0;
+        if (s1 < ns) {
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bar[st ^ 1], (uint32_t)(e1 - o1) * 16u);
+                if (e1 > o1) bulk_g2s(buf + (st ^ 1) * kNarrowStage, A.aa + o1, (uint32_t)(e1 - o1) * 16u, &bar[st ^ 1], pol);
+            }
+            const int W1 = (int)((e1 - o1) / kSlice);
+#pragma unroll
+            for (int q = 0; q < kNarrowMax; ++q) jn[q] = q < W1 ? __ldcs(A.ja + o1 + 32 * q + lane) : 0;
+            ln = s1 * kSlice + lane < A.n_rows ? (int)A.rowlen[s1 * kSlice + lane] : 0;
+        } else {
+#pragma unroll
+            for (int q = 0; q < kNarrowMax; ++q) jn[q] = 0;
+        }
+        // the current slice
+        mbar_wait(&bar[st], (k >> 1) & 1);
+        const double2* sa = reinterpret_cast<const double2*>(buf + st * kNarrowStage) + lane;
+        const int W = (int)((e0 - o0) / kSlice);
+        RowSum acc;
+        acc.init(lc);
+#pragma unroll
+        for (int q = 0; q < kNarrowMax; ++q) acc.add(q, spmv_prod(A, q < W ? sa[32 * q] : z, xs[q]));
+        const int64_t row = s * kSlice + lane;
+        if (row < A.n_rows) {
+            double2 v[1] = {acc.result()}, sv[1], tc[1];
+            double tr[1];
+            body.row(row, v, sv, tc, tr);
+        }
+        __syncwarp();  // every lane has read stage st before it is refilled
+        o0 = o1;
+        e0 = e1;
+        o1 = o2;
+        e1 = e2;
+        lc = ln;
+#pragma unroll
+        for (int q = 0; q < kNarrowMax; ++q) jc[q] = jn[q];
+    }
+}
+
+template <class Body>
+__device__ __forceinline__ void narrow_dispatch(const SellView& A, const double2* __restrict__ x, Body& body,
+                                                unsigned char* smem) {
+    if (A.narrow_tma) narrow_tma_run(A, x, body, smem);
+    else narrow_run(A, x, body);
+}
+
+__host__ __forceinline__ unsigned narrow_grid(const SellView& v) {
+    if (v.narrow_tma) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t want = (int64_t)sms * ZK_NARROW_MINB;
+        const int64_t need = (v.nslices + kNarrowWarps - 1) / kNarrowWarps;
+        return (unsigned)(need < want ? (need > 0 ? need : 1) : want);
+    }
+    return (unsigned)((v.nslices * kSlice + kNarrowThreads - 1) / kNarrowThreads);
+}
+__host__ __forceinline__ size_t narrow_smem(const SellView& v) { return v.narrow_tma ? kNarrowSmem : 0; }
 
 // Index of long row `row` in the side CSR (binary search in its block's range).
 __device__ __forceinline__ int long_index(const SellView& A, int64_t blk, int64_t row) {
