@@ -188,6 +188,7 @@ def algorithmic_bytes(n: int, nnz: int):
     return {
         "spmv": A,
         "spmv_pivot": A,                      # v = A p^ (plain pipeline)
+        "spmv2": A + 32 * n,                  # narrow matrices: t = A x and v = A p^ in one matrix pass
         "res_pass": 32 * n,                   # ||b - A x||: b, A x
         "pivot_first": A,
         "pivot_dot": 32 * n,                  # <r~, v>: r~, v
@@ -302,12 +303,12 @@ def run_zk(args, dist: Dist):
                 entry["gbs"] = round(B[name] / (avg * 1e-3) / 1e9, 1)
             phases[name] = entry
     body = [p for p in ("s_update", "x_alpha", "true_res_s", "spmv_t", "tt_ts", "xr_update", "true_res", "res_pass",
-                        "p_next", "spmv_pivot", "pivot_dot")
+                        "p_next", "spmv_pivot", "pivot_dot", "spmv2")
             if p in phases]
     # matrices at most 8 entries wide (no long rows) run the narrow SpMV kernels (zk_spmv.cuh)
     spmv_k = "k_spmv_phase_narrow" if int(np.diff(ia).max()) <= 8 and os.environ.get("ZK_NARROW") != "0" \
         else "k_spmv_phase"
-    kernel_names = {"spmv_t": spmv_k, "spmv_pivot": spmv_k, "true_res": spmv_k,
+    kernel_names = {"spmv_t": spmv_k, "spmv_pivot": spmv_k, "true_res": spmv_k, "spmv2": "k_spmv2_phase_narrow",
                     "res_pass": "k_res_pass",
                     "s_update": "k_s_update_pipe", "xr_update": "k_xr_update_pipe", "tt_ts": "k_tt_ts_pass",
                     "pivot_dot": "k_pivot_pass", "p_next": "k_p_next"}

@@ -92,8 +92,9 @@ zk_status zk_event_elapsed(zk_context* ctx, int start_slot, int stop_slot, doubl
  * returns the accumulated device time and launch count per phase, in this
  * order: setup, p_first, pivot_first, pivot_first_dot, s_update, x_alpha,
  * true_res_s, spmv_t, tt_ts, xr_update, true_res (A x), res_pass, p_next,
- * spmv_pivot, pivot_dot. */
-#define ZK_NPHASES 15
+ * spmv_pivot, pivot_dot, spmv2 (matrices at most 8 entries wide: A x and A p^
+ * in one pass, replacing true_res and spmv_pivot). */
+#define ZK_NPHASES 16
 zk_status zk_profile_enable(zk_context* ctx, int on);
 zk_status zk_profile_read(zk_context* ctx, double* total_ms, int64_t* launches);
 

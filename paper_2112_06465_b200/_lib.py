@@ -202,7 +202,7 @@ def launch_count() -> int:
 
 
 PHASES = ("setup", "p_first", "pivot_first", "pivot_first_dot", "s_update", "x_alpha", "true_res_s", "spmv_t",
-          "tt_ts", "xr_update", "true_res", "res_pass", "p_next", "spmv_pivot", "pivot_dot")
+          "tt_ts", "xr_update", "true_res", "res_pass", "p_next", "spmv_pivot", "pivot_dot", "spmv2")
 
 
 def event_record(slot: int) -> None:

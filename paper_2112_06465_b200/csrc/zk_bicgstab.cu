@@ -222,6 +222,31 @@ __global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW_MINB) k_spmv_phase_n
     narrow_dispatch(A, x, body, smem);
 }
 
+// Narrow matrices: K61's A x and K2's A p^ in one pass over the matrix
+// (t = A x, v = A p^); the loop body runs Kp before it (launch_body).
+struct PhaseSpmv2Body {
+    static constexpr int kNC = 0, kNR = 0, kSV = 0;
+    double2* __restrict__ y0;
+    double2* __restrict__ y1;
+    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[2], const double2 (&)[1], double2 (&)[1],
+                                        double (&)[1]) {
+        y0[r] = v[0];
+        y1[r] = v[1];
+    }
+};
+
+#ifndef ZK_NARROW2_MINB
+#define ZK_NARROW2_MINB 2  // 128 registers, no spills: 16 warps per SM (1 CTA at 144 registers: 857 vs 589 us on C5)
+#endif
+__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW2_MINB)
+    k_spmv2_phase_narrow(SellView A, const double2* __restrict__ x0, const double2* __restrict__ x1,
+                         double2* __restrict__ y0, double2* __restrict__ y1, const SolverState* st) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (st->done) return;
+    PhaseSpmv2Body body{y0, y1};
+    narrow_tma_run<2>(A, x0, x1, body, smem);
+}
+
 // ---- K2 pass: <r~, v> -> pivot, alpha (krylov.py:268-271) ----
 // Last kernel of the loop body: sets the graph's WHILE condition (the
 // prologue instance, use_cond = 0, runs the first iteration's K2).
@@ -520,6 +545,7 @@ struct Launch {
     size_t smem_l1s = 0, smem_l1x = 0, smem_l1p = 0, smem_l1t = 0;
     unsigned grid_l1s = 0, grid_l1x = 0, grid_l1p = 0, grid_l1t = 0;
     SellView Apl;             // plain SpMV phases (K2, K4, K61 products)
+    bool fuse2;               // narrow matrices: K61 + K2 products in one pass (PH_SPMV2)
     size_t smem_pl = 0;
     L1View l1r;               // true-residual pass
     size_t smem_l1r = 0;
@@ -533,6 +559,7 @@ enum Phase : int {
     PH_SETUP, PH_P_FIRST, PH_PIVOT_FIRST, PH_PIVOT_FIRST_DOT,          // prologue
     PH_S_UPDATE, PH_X_ALPHA, PH_TRUE_RES_S, PH_SPMV_T, PH_TT_TS, PH_XR_UPDATE,
     PH_TRUE_RES, PH_RES_PASS, PH_P_NEXT, PH_SPMV_PIVOT, PH_PIVOT_DOT,
+    PH_SPMV2,  // narrow matrices: t = A x and v = A p^ in one pass
     PH_COUNT
 };
 
@@ -595,6 +622,23 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     { PhaseScope ps(pe, PH_SPMV_T); spmv_phase(L, s, B.sh, B.t, B.st); }
     { PhaseScope ps(pe, PH_TT_TS); k_tt_ts_pass<<<L.grid_l1t, kL1Threads, L.smem_l1t, s>>>(B, L.l1t); }
     { PhaseScope ps(pe, PH_XR_UPDATE); k_xr_update_pipe<<<L.grid_l1x, kL1Threads, L.smem_l1x, s>>>(B, L.l1x); }
+    if (L.fuse2) {
+        // Kp first (it reads v and writes p, p^ only; the residual pass's
+        // stop decision only ever skips it, and p is not part of the result),
+        // then t = A x and v = A p^ in one matrix pass, then both passes
+        { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
+        {
+            PhaseScope ps(pe, PH_SPMV2);
+            k_spmv2_phase_narrow<<<narrow_grid(L.Apl), kNarrowThreads, kNarrowSmem, s>>>(L.Apl, B.x, B.ph, B.t, B.v,
+                                                                                         B.st);
+        }
+        { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
+        {
+            PhaseScope ps(pe, PH_PIVOT_DOT);
+            k_pivot_pass<<<L.grid_l1p, kL1Threads, L.smem_l1p, s>>>(B, L.l1p, cond, use_cond);
+        }
+        return;
+    }
     { PhaseScope ps(pe, PH_TRUE_RES); spmv_phase(L, s, B.x, B.t, B.st); }
     { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
     { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
@@ -605,7 +649,7 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
     }
 }
 // launches per loop trip
-inline int body_kernels(const Launch&) { return 11; }
+inline int body_kernels(const Launch& L) { return L.fuse2 ? 10 : 11; }
 
 void accumulate(zk_context* c, PhaseEvents& pe) {
     for (int k = 0; k < PH_COUNT; ++k) {
@@ -623,6 +667,7 @@ void set_attrs(const Launch& L) {
     smem_attr(k_setup, L.smem_s);
     smem_attr(k_spmv_phase, L.smem_pl);
     smem_attr(k_spmv_phase_narrow, kNarrowSmem);
+    smem_attr(k_spmv2_phase_narrow, kNarrowSmem);
     smem_attr(k_res_pass, L.smem_l1r);
     smem_attr(k_pivot_pass, L.smem_l1p);
     smem_attr(k_tt_ts_pass, L.smem_l1t);
@@ -733,6 +778,10 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.Ar.sv[0] = B.b;
     L.Apl = sell_view(A, c, 0, 0);
     L.ppg = plain_grid(A, L.Apl);
+    {
+        const char* e = std::getenv("ZK_FUSE2");  // A/B switch (experiments only)
+        L.fuse2 = L.Apl.narrow_tma && !(e && e[0] == '0');
+    }
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_pl = pipe_smem_bytes(L.Apl, 0);
     L.smem_r = pipe_smem_bytes(L.Ar, ex_r);

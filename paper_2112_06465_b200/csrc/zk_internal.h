@@ -101,8 +101,8 @@ struct zk_context {
     int64_t launches = 0;          // kernels launched by this context
     cudaEvent_t events[32] = {};   // zk_event_record slots
     bool profile = false;          // zk_profile_enable
-    double prof_ms[16] = {};
-    int64_t prof_n[16] = {};
+    double prof_ms[32] = {};  // >= ZK_NPHASES
+    int64_t prof_n[32] = {};
     std::mutex mu;
 
     char* plan(int32_t L, int32_t kind);

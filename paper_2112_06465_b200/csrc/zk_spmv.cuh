@@ -648,9 +648,11 @@ constexpr int kNarrowWarps = kNarrowThreads / 32;
 constexpr int kNarrowStage = kNarrowMax * kSlice * 16;  // values of one slice
 constexpr int kNarrowSmem = 128 + kNarrowWarps * 2 * kNarrowStage;
 
-template <class Body>
-__device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2* __restrict__ x, Body& body,
-                                               unsigned char* smem) {
+// NX = 2: rows of A x0 and A x1 from one pass over the matrix (both gather
+// sets in flight, the two sums one after the other).
+template <int NX, class Body>
+__device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2* __restrict__ x0,
+                                               const double2* __restrict__ x1, Body& body, unsigned char* smem) {
     static_assert(Body::kSV == 0 && Body::kNC == 0 && Body::kNR == 0, "plain bodies only");
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
@@ -684,9 +686,13 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
     }
     for (uint32_t k = 0; s < ns; s = s1, s1 += nw, ++k) {
         const int st = (int)(k & 1);
-        double2 xs[kNarrowMax];
+        double2 xs[NX][kNarrowMax];
 #pragma unroll
-        for (int q = 0; q < kNarrowMax; ++q) xs[q] = q < lc ? __ldg(x + jc[q]) : z;
+        for (int q = 0; q < kNarrowMax; ++q) xs[0][q] = q < lc ? __ldg(x0 + jc[q]) : z;
+        if constexpr (NX == 2) {
+#pragma unroll
+            for (int q = 0; q < kNarrowMax; ++q) xs[NX - 1][q] = q < lc ? __ldg(x1 + jc[q]) : z;
+        }
         // the next slice: values by TMA into the other stage, columns and
         // lengths into registers; offsets of the one after
         const int64_t s2 = s1 + nw;
@@ -710,13 +716,18 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
         mbar_wait(&bar[st], (k >> 1) & 1);
         const double2* sa = reinterpret_cast<const double2*>(buf + st * kNarrowStage) + lane;
         const int W = (int)((e0 - o0) / kSlice);
-        RowSum acc;
-        acc.init(lc);
+        double2 v[NX];
 #pragma unroll
-        for (int q = 0; q < kNarrowMax; ++q) acc.add(q, spmv_prod(A, q < W ? sa[32 * q] : z, xs[q]));
+        for (int u = 0; u < NX; ++u) {
+            RowSum acc;
+            acc.init(lc);
+#pragma unroll
+            for (int q = 0; q < kNarrowMax; ++q) acc.add(q, spmv_prod(A, q < W ? sa[32 * q] : z, xs[u][q]));
+            v[u] = acc.result();
+        }
         const int64_t row = s * kSlice + lane;
         if (row < A.n_rows) {
-            double2 v[1] = {acc.result()}, sv[1], tc[1];
+            double2 sv[1], tc[1];
             double tr[1];
             body.row(row, v, sv, tc, tr);
         }
@@ -734,7 +745,7 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
 template <class Body>
 __device__ __forceinline__ void narrow_dispatch(const SellView& A, const double2* __restrict__ x, Body& body,
                                                 unsigned char* smem) {
-    if (A.narrow_tma) narrow_tma_run(A, x, body, smem);
+    if (A.narrow_tma) narrow_tma_run<1>(A, x, x, body, smem);
     else narrow_run(A, x, body);
 }
 
