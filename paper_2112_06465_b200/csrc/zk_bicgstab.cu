@@ -213,13 +213,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_phase(SellView A, cons
     sell_run<1>(A, x, nullptr, body, R, smem);
 }
 
-__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW_MINB) k_spmv_phase_narrow(SellView A, const double2* __restrict__ x,
-                                                                          double2* __restrict__ y,
-                                                                          const SolverState* st) {
+template <int WM>
+__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
+    k_spmv_phase_narrow(SellView A, const double2* __restrict__ x, double2* __restrict__ y, const SolverState* st) {
+    extern __shared__ __align__(128) unsigned char smem[];
     if (st->done) return;
     PhaseSpmvBody body{y};
-    extern __shared__ __align__(128) unsigned char smem[];
-    narrow_dispatch(A, x, body, smem);
+    narrow_tma_run<WM, 1>(A, x, x, body, smem);
 }
 
 // Narrow matrices: K61's A x and K2's A p^ in one pass over the matrix
@@ -235,16 +235,26 @@ struct PhaseSpmv2Body {
     }
 };
 
-#ifndef ZK_NARROW2_MINB
-#define ZK_NARROW2_MINB 2  // 128 registers, no spills: 16 warps per SM (1 CTA at 144 registers: 857 vs 589 us on C5)
-#endif
-__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW2_MINB)
+template <int WM>
+__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB2)
     k_spmv2_phase_narrow(SellView A, const double2* __restrict__ x0, const double2* __restrict__ x1,
                          double2* __restrict__ y0, double2* __restrict__ y1, const SolverState* st) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (st->done) return;
     PhaseSpmv2Body body{y0, y1};
-    narrow_tma_run<2>(A, x0, x1, body, smem);
+    narrow_tma_run<WM, 2>(A, x0, x1, body, smem);
+}
+
+// Wide matrices (experiment, ZK_FUSE2=2): the same two products through the ring.
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spmv2_phase(SellView A, const double2* __restrict__ x0,
+                                                                 const double2* __restrict__ x1,
+                                                                 double2* __restrict__ y0, double2* __restrict__ y1,
+                                                                 const SolverState* st) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (st->done) return;
+    PhaseSpmv2Body body{y0, y1};
+    const RedCfg R{};
+    sell_run<2>(A, x0, x1, body, R, smem);
 }
 
 // ---- K2 pass: <r~, v> -> pivot, alpha (krylov.py:268-271) ----
@@ -592,9 +602,9 @@ struct PhaseScope {
     }
 };
 
-// A plain SpMV phase: the direct kernel for narrow matrices, else the ring.
+// A plain SpMV phase: the narrow kernels for matrices at most 16 wide, else the ring.
 inline void spmv_phase(const Launch& L, cudaStream_t s, const double2* x, double2* y, const SolverState* st) {
-    if (L.Apl.narrow) k_spmv_phase_narrow<<<narrow_grid(L.Apl), kNarrowThreads, narrow_smem(L.Apl), s>>>(L.Apl, x, y, st);
+    if (L.Apl.narrow_w) ZK_NARROW_LAUNCH(k_spmv_phase_narrow, L.Apl, 1, s, L.Apl, x, y, st);
     else k_spmv_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, x, y, st);
 }
 
@@ -629,8 +639,10 @@ void launch_body(const Launch& L, cudaStream_t s, cudaGraphConditionalHandle con
         { PhaseScope ps(pe, PH_P_NEXT); k_p_next<<<L.ew, 256, 0, s>>>(B); }
         {
             PhaseScope ps(pe, PH_SPMV2);
-            k_spmv2_phase_narrow<<<narrow_grid(L.Apl), kNarrowThreads, kNarrowSmem, s>>>(L.Apl, B.x, B.ph, B.t, B.v,
-                                                                                         B.st);
+            if (L.Apl.narrow_w)
+                ZK_NARROW_LAUNCH(k_spmv2_phase_narrow, L.Apl, 2, s, L.Apl, B.x, B.ph, B.t, B.v, B.st);
+            else
+                k_spmv2_phase<<<L.ppg, kPipeThreads, L.smem_pl, s>>>(L.Apl, B.x, B.ph, B.t, B.v, B.st);
         }
         { PhaseScope ps(pe, PH_RES_PASS); k_res_pass<<<L.grid_l1r, kL1Threads, L.smem_l1r, s>>>(B, L.l1r); }
         {
@@ -666,8 +678,9 @@ void accumulate(zk_context* c, PhaseEvents& pe) {
 void set_attrs(const Launch& L) {
     smem_attr(k_setup, L.smem_s);
     smem_attr(k_spmv_phase, L.smem_pl);
-    smem_attr(k_spmv_phase_narrow, kNarrowSmem);
-    smem_attr(k_spmv2_phase_narrow, kNarrowSmem);
+    ZK_NARROW_ATTR(k_spmv_phase_narrow);
+    ZK_NARROW_ATTR(k_spmv2_phase_narrow);
+    smem_attr(k_spmv2_phase, L.smem_pl);
     smem_attr(k_res_pass, L.smem_l1r);
     smem_attr(k_pivot_pass, L.smem_l1p);
     smem_attr(k_tt_ts_pass, L.smem_l1t);
@@ -780,7 +793,7 @@ static Launch make_launch(zk_context* c, zk_csr* A, SolverPlan* P) {
     L.ppg = plain_grid(A, L.Apl);
     {
         const char* e = std::getenv("ZK_FUSE2");  // A/B switch (experiments only)
-        L.fuse2 = L.Apl.narrow_tma && !(e && e[0] == '0');
+        L.fuse2 = (L.Apl.narrow_w && !(e && e[0] == '0')) || (e && e[0] == '2');
     }
     L.smem_s = pipe_smem_bytes(L.As, ex_s);
     L.smem_pl = pipe_smem_bytes(L.Apl, 0);

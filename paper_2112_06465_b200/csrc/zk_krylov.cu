@@ -217,11 +217,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_kspmv(SellView A, const dou
     sell_run<1>(A, x, nullptr, body, R, smem);
 }
 
-__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW_MINB) k_kspmv_narrow(SellView A, const double2* __restrict__ x,
-                                                                     KPlainBody body, Gate gate) {
-    if (gate.skip()) return;
+template <int WM>
+__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
+    k_kspmv_narrow(SellView A, const double2* __restrict__ x, KPlainBody body, Gate gate) {
     extern __shared__ __align__(128) unsigned char smem[];
-    narrow_dispatch(A, x, body, smem);
+    if (gate.skip()) return;
+    narrow_tma_run<WM, 1>(A, x, x, body, smem);
 }
 
 // ---- elementwise kernels -------------------------------------------------------
@@ -556,9 +557,9 @@ struct KLaunch {
     void spmv(const double2* x, double2* y, double2* y2, Gate g) {
         SellView v = sell_view(A, c, 0, 0);
         const unsigned grid = plain_grid(A, v);
-        if (v.narrow) {
-            ZK_CUDA(cudaFuncSetAttribute(k_kspmv_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, kNarrowSmem));
-            k_kspmv_narrow<<<narrow_grid(v), kNarrowThreads, narrow_smem(v), s>>>(v, x, KPlainBody{y, y2}, g);
+        if (v.narrow_w) {
+            ZK_NARROW_ATTR(k_kspmv_narrow);
+            ZK_NARROW_LAUNCH(k_kspmv_narrow, v, 1, s, v, x, KPlainBody{y, y2}, g);
             check();
             return;
         }

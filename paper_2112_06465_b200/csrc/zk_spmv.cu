@@ -15,8 +15,7 @@ namespace zk {
 // shared memory after the ring (epilogue stash, reduction nodes).
 SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) {
     SellView v;
-    v.narrow = false;
-    v.narrow_tma = false;
+    v.narrow_w = 0;
     v.sv[0] = v.sv[1] = nullptr;
     v.n_rows = A->n_rows;
     v.n_cols = A->n_cols;
@@ -118,9 +117,10 @@ unsigned plain_grid(const zk_csr* A, SellView& v) {
     v.spb = (int32_t)spb;
     v.nvb = (A->nslices + spb - 1) / spb;
     {
-        const char* e = std::getenv("ZK_NARROW");  // A/B switch (experiments only)
-        v.narrow = A->wmax <= kNarrowMax && A->n_long == 0 && !(e && e[0] == '0');
-        v.narrow_tma = v.narrow && !(e && e[0] == '1');
+        // A/B switch (experiments only): "0" the ring only, "8" no width-16 class
+        const char* e = std::getenv("ZK_NARROW");
+        const int cap = (e && e[0] == '0') ? 0 : (e && e[0] == '8') ? 8 : 16;
+        v.narrow_w = (A->n_long == 0 && A->wmax <= cap) ? (A->wmax <= 8 ? 8 : 16) : 0;
     }
     const int64_t g = v.nvb < num_sms() ? v.nvb : num_sms();
     return (unsigned)(g > 0 ? g : 1);
@@ -229,11 +229,12 @@ struct PlainSpmv {
     __device__ __forceinline__ void finish(const double*) {}
 };
 
-__global__ void __launch_bounds__(kNarrowThreads, ZK_NARROW_MINB) k_spmv_narrow(SellView A, const double2* __restrict__ x,
-                                                                    double2* __restrict__ y) {
-    PlainSpmv body{y};
+template <int WM>
+__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
+    k_spmv_narrow(SellView A, const double2* __restrict__ x, double2* __restrict__ y) {
     extern __shared__ __align__(128) unsigned char smem[];
-    narrow_dispatch(A, x, body, smem);
+    PlainSpmv body{y};
+    narrow_tma_run<WM, 1>(A, x, x, body, smem);
 }
 
 __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv(SellView A, const double2* __restrict__ x,
@@ -570,9 +571,9 @@ void spmv_device(zk_context* c, const zk_csr* A, const double2* x, double2* y) {
     }
     SellView v = sell_view(A, c, 0, 0);
     const unsigned grid = plain_grid(A, v);
-    if (v.narrow) {
-        ZK_CUDA(cudaFuncSetAttribute(k_spmv_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, kNarrowSmem));
-        k_spmv_narrow<<<narrow_grid(v), kNarrowThreads, narrow_smem(v), c->stream>>>(v, x, y);
+    if (v.narrow_w) {
+        ZK_NARROW_ATTR(k_spmv_narrow);
+        ZK_NARROW_LAUNCH(k_spmv_narrow, v, 1, c->stream, v, x, y);
         ZK_CUDA(cudaGetLastError());
         c->launches++;
         return;

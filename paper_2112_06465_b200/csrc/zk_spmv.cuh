@@ -101,8 +101,7 @@ struct SellView {
     bool prefetch;        // L2 bulk prefetch of each slice's new x rows (one more TMA op per slice)
     bool swap;            // numpy elided the gathered temporary: prod = F1(x[ja], aa)
     bool fma;
-    bool narrow;          // plain launches: direct kernel (narrow_run) instead of the ring
-    bool narrow_tma;      // ... its per-warp TMA double-buffered variant (narrow_tma_run)
+    int32_t narrow_w;     // plain launches: 8 / 16 = narrow kernels of that width class, 0 = the ring
 };
 
 __device__ __forceinline__ double2 spmv_prod(const SellView& A, double2 a, double2 xv) {
@@ -591,72 +590,42 @@ __device__ __forceinline__ RowVals<NX> row_fast_dispatch(int W, const double2* _
     }
 }
 
-// ---- narrow matrices: one thread per row, 16 warps per SM ----------------
-// Every slice at most kNarrowMax wide and no long rows (C1/C5's 7-point
-// rows).  With 7-entry rows the ring's consumers (7 warps per SM) have too
-// few gathers in flight (C5 SpMV 648 us, 0.68 of HBM).  Default: the per-warp
-// TMA variant (narrow_tma_run, C5 421 us); narrow_run (direct loads, one warp
-// per slice, no prefetch: 509 us at 24 warps per SM) stays as ZK_NARROW=1 for
-// A/B.  Both sum in numpy's order (RowSum, the fast path's order).
-constexpr int kNarrowMax = 8;
+// ---- narrow matrices: one thread per row, per-warp TMA double buffer ------
+// Slices at most 8 (C1/C5's 7-point rows) or 16 (C3's P1 elements) wide and
+// no long rows.  With short rows the ring's consumers (7 warps per SM) have
+// too few gathers in flight (C5 SpMV 648 us, 0.68 of HBM).  Here a persistent
+// warp walks slices s, s + nw, ...: the next slice's values arrive by one
+// bulk copy into the warp's other stage and its columns and row lengths by
+// loads into registers while the current slice's gathers are in flight, so
+// only the gathers' latency is exposed (C5: 421 us; one warp per slice with
+// direct loads and no prefetch measured 509 us).  Rows sum in numpy's order
+// (RowSum, the fast path's order).
 constexpr int kNarrowThreads = 256;
-#ifndef ZK_NARROW_MINB
-#define ZK_NARROW_MINB 2  // resident CTAs per SM (108 registers, no spills; 3 CTAs spill at 80)
-#endif
-#ifndef ZK_NARROW_LD
-#define ZK_NARROW_LD __ldcs
-#endif
-
-template <class Body>
-__device__ __forceinline__ void narrow_run(const SellView& A, const double2* __restrict__ x, Body& body) {
-    static_assert(Body::kSV == 0 && Body::kNC == 0 && Body::kNR == 0, "plain bodies only");
-    const int lane = threadIdx.x & 31;
-    const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (s >= A.nslices) return;
-    const int64_t off = A.slice_off[s];
-    const int W = (int)((A.slice_off[s + 1] - off) / kSlice);
-    const int64_t row = s * kSlice + lane;
-    const bool mine = row < A.n_rows;
-    const int len = mine ? (int)A.rowlen[row] : 0;
-    const int32_t* sja = A.ja + off + lane;
-    const double2* saa = A.aa + off + lane;
-    int32_t j[kNarrowMax];
-    double2 a[kNarrowMax], xs[kNarrowMax];
-    const double2 z = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int k = 0; k < kNarrowMax; ++k) j[k] = k < W ? ZK_NARROW_LD(sja + 32 * k) : 0;
-#pragma unroll
-    for (int k = 0; k < kNarrowMax; ++k) a[k] = k < W ? ZK_NARROW_LD(saa + 32 * k) : z;
-#pragma unroll
-    for (int k = 0; k < kNarrowMax; ++k) xs[k] = k < len ? __ldg(x + j[k]) : z;
-    RowSum acc;
-    acc.init(len);
-#pragma unroll
-    for (int k = 0; k < kNarrowMax; ++k) acc.add(k, spmv_prod(A, a[k], xs[k]));
-    if (mine) {
-        double2 v[1] = {acc.result()}, sv[1], tc[1];
-        double tr[1];
-        body.row(row, v, sv, tc, tr);
-    }
-}
-
-// Per-warp TMA variant: a persistent warp walks slices s, s + nw, ...; the
-// next slice's values arrive by one bulk copy into the warp's other stage
-// and its columns and row lengths by loads into registers while the current
-// slice's gathers are in flight, so only the gathers' latency is exposed.
 constexpr int kNarrowWarps = kNarrowThreads / 32;
-constexpr int kNarrowStage = kNarrowMax * kSlice * 16;  // values of one slice
-constexpr int kNarrowSmem = 128 + kNarrowWarps * 2 * kNarrowStage;
+#ifndef ZK_NARROW_MINB
+#define ZK_NARROW_MINB 2  // width 8: CTAs per SM (108 registers, no spills; 3 CTAs spill at 80)
+#endif
+#ifndef ZK_NARROW2_MINB
+#define ZK_NARROW2_MINB 2  // width 8, two vectors: 128 registers, no spills (1 CTA at 144: 857 vs 589 us on C5)
+#endif
+template <int WM>
+struct NarrowCfg {
+    static constexpr int kStage = WM * kSlice * 16;  // values of one slice
+    static constexpr int kSmem = 128 + kNarrowWarps * 2 * kStage;
+    static constexpr int kMinB = WM <= 8 ? ZK_NARROW_MINB : 1;    // one vector
+    static constexpr int kMinB2 = WM <= 8 ? ZK_NARROW2_MINB : 1;  // two vectors
+};
 
 // NX = 2: rows of A x0 and A x1 from one pass over the matrix (both gather
 // sets in flight, the two sums one after the other).
-template <int NX, class Body>
+template <int WM, int NX, class Body>
 __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2* __restrict__ x0,
                                                const double2* __restrict__ x1, Body& body, unsigned char* smem) {
     static_assert(Body::kSV == 0 && Body::kNC == 0 && Body::kNR == 0, "plain bodies only");
+    constexpr int kStage = NarrowCfg<WM>::kStage;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
-    unsigned char* buf = smem + 128 + (size_t)warp * 2 * kNarrowStage;
+    unsigned char* buf = smem + 128 + (size_t)warp * 2 * kStage;
     const int64_t ns = A.nslices, nw = (int64_t)gridDim.x * kNarrowWarps;
     int64_t s = (int64_t)blockIdx.x * kNarrowWarps + warp;
     if (s >= ns) return;
@@ -676,45 +645,45 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
         mbar_arrive_expect_tx(&bar[0], (uint32_t)(e0 - o0) * 16u);
         if (e0 > o0) bulk_g2s(buf, A.aa + o0, (uint32_t)(e0 - o0) * 16u, &bar[0], pol);
     }
-    int32_t jc[kNarrowMax];
+    int32_t jc[WM];
     int lc;
     {
         const int W = (int)((e0 - o0) / kSlice);
 #pragma unroll
-        for (int q = 0; q < kNarrowMax; ++q) jc[q] = q < W ? __ldcs(A.ja + o0 + 32 * q + lane) : 0;
+        for (int q = 0; q < WM; ++q) jc[q] = q < W ? __ldcs(A.ja + o0 + 32 * q + lane) : 0;
         lc = s * kSlice + lane < A.n_rows ? (int)A.rowlen[s * kSlice + lane] : 0;
     }
     for (uint32_t k = 0; s < ns; s = s1, s1 += nw, ++k) {
         const int st = (int)(k & 1);
-        double2 xs[NX][kNarrowMax];
+        double2 xs[NX][WM];
 #pragma unroll
-        for (int q = 0; q < kNarrowMax; ++q) xs[0][q] = q < lc ? __ldg(x0 + jc[q]) : z;
+        for (int q = 0; q < WM; ++q) xs[0][q] = q < lc ? __ldg(x0 + jc[q]) : z;
         if constexpr (NX == 2) {
 #pragma unroll
-            for (int q = 0; q < kNarrowMax; ++q) xs[NX - 1][q] = q < lc ? __ldg(x1 + jc[q]) : z;
+            for (int q = 0; q < WM; ++q) xs[NX - 1][q] = q < lc ? __ldg(x1 + jc[q]) : z;
         }
         // the next slice: values by TMA into the other stage, columns and
         // lengths into registers; offsets of the one after
         const int64_t s2 = s1 + nw;
         const int64_t o2 = s2 < ns ? A.slice_off[s2] : 0, e2 = s2 < ns ? A.slice_off[s2 + 1] : 0;
-        int32_t jn[kNarrowMax];
+        int32_t jn[WM];
         int ln = 0;
         if (s1 < ns) {
             if (lane == 0) {
                 mbar_arrive_expect_tx(&bar[st ^ 1], (uint32_t)(e1 - o1) * 16u);
-                if (e1 > o1) bulk_g2s(buf + (st ^ 1) * kNarrowStage, A.aa + o1, (uint32_t)(e1 - o1) * 16u, &bar[st ^ 1], pol);
+                if (e1 > o1) bulk_g2s(buf + (st ^ 1) * kStage, A.aa + o1, (uint32_t)(e1 - o1) * 16u, &bar[st ^ 1], pol);
             }
             const int W1 = (int)((e1 - o1) / kSlice);
 #pragma unroll
-            for (int q = 0; q < kNarrowMax; ++q) jn[q] = q < W1 ? __ldcs(A.ja + o1 + 32 * q + lane) : 0;
+            for (int q = 0; q < WM; ++q) jn[q] = q < W1 ? __ldcs(A.ja + o1 + 32 * q + lane) : 0;
             ln = s1 * kSlice + lane < A.n_rows ? (int)A.rowlen[s1 * kSlice + lane] : 0;
         } else {
 #pragma unroll
-            for (int q = 0; q < kNarrowMax; ++q) jn[q] = 0;
+            for (int q = 0; q < WM; ++q) jn[q] = 0;
         }
         // the current slice
         mbar_wait(&bar[st], (k >> 1) & 1);
-        const double2* sa = reinterpret_cast<const double2*>(buf + st * kNarrowStage) + lane;
+        const double2* sa = reinterpret_cast<const double2*>(buf + st * kStage) + lane;
         const int W = (int)((e0 - o0) / kSlice);
         double2 v[NX];
 #pragma unroll
@@ -722,7 +691,7 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
             RowSum acc;
             acc.init(lc);
 #pragma unroll
-            for (int q = 0; q < kNarrowMax; ++q) acc.add(q, spmv_prod(A, q < W ? sa[32 * q] : z, xs[u][q]));
+            for (int q = 0; q < WM; ++q) acc.add(q, spmv_prod(A, q < W ? sa[32 * q] : z, xs[u][q]));
             v[u] = acc.result();
         }
         const int64_t row = s * kSlice + lane;
@@ -738,29 +707,39 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
         e1 = e2;
         lc = ln;
 #pragma unroll
-        for (int q = 0; q < kNarrowMax; ++q) jc[q] = jn[q];
+        for (int q = 0; q < WM; ++q) jc[q] = jn[q];
     }
 }
 
-template <class Body>
-__device__ __forceinline__ void narrow_dispatch(const SellView& A, const double2* __restrict__ x, Body& body,
-                                                unsigned char* smem) {
-    if (A.narrow_tma) narrow_tma_run<1>(A, x, x, body, smem);
-    else narrow_run(A, x, body);
+// Persistent grid of a narrow launch (NX vectors).
+__host__ __forceinline__ unsigned narrow_grid(const SellView& v, int nx = 1) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int minb = v.narrow_w <= 8 ? (nx == 1 ? NarrowCfg<8>::kMinB : NarrowCfg<8>::kMinB2)
+                                     : (nx == 1 ? NarrowCfg<16>::kMinB : NarrowCfg<16>::kMinB2);
+    const int64_t want = (int64_t)sms * minb;
+    const int64_t need = (v.nslices + kNarrowWarps - 1) / kNarrowWarps;
+    return (unsigned)(need < want ? (need > 0 ? need : 1) : want);
+}
+__host__ __forceinline__ size_t narrow_smem(const SellView& v) {
+    return v.narrow_w <= 8 ? NarrowCfg<8>::kSmem : NarrowCfg<16>::kSmem;
 }
 
-__host__ __forceinline__ unsigned narrow_grid(const SellView& v) {
-    if (v.narrow_tma) {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t want = (int64_t)sms * ZK_NARROW_MINB;
-        const int64_t need = (v.nslices + kNarrowWarps - 1) / kNarrowWarps;
-        return (unsigned)(need < want ? (need > 0 ? need : 1) : want);
-    }
-    return (unsigned)((v.nslices * kSlice + kNarrowThreads - 1) / kNarrowThreads);
-}
-__host__ __forceinline__ size_t narrow_smem(const SellView& v) { return v.narrow_tma ? kNarrowSmem : 0; }
+// Launch kernel template KERN<8> or KERN<16> by the view's narrow width.
+#define ZK_NARROW_LAUNCH(KERN, V, NX, STREAM, ...)                                                         \
+    do {                                                                                                  \
+        if ((V).narrow_w <= 8)                                                                            \
+            KERN<8><<<narrow_grid((V), (NX)), kNarrowThreads, narrow_smem(V), (STREAM)>>>(__VA_ARGS__);  \
+        else                                                                                              \
+            KERN<16><<<narrow_grid((V), (NX)), kNarrowThreads, narrow_smem(V), (STREAM)>>>(__VA_ARGS__); \
+    } while (0)
+// Dynamic shared memory attributes of both instantiations.
+#define ZK_NARROW_ATTR(KERN)                                                                                     \
+    do {                                                                                                        \
+        ZK_CUDA(cudaFuncSetAttribute(KERN<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, NarrowCfg<8>::kSmem));   \
+        ZK_CUDA(cudaFuncSetAttribute(KERN<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, NarrowCfg<16>::kSmem)); \
+    } while (0)
 
 // Index of long row `row` in the side CSR (binary search in its block's range).
 __device__ __forceinline__ int long_index(const SellView& A, int64_t blk, int64_t row) {

@@ -304,29 +304,38 @@ def test_solver_graph_follows_arithmetic_changes():
 
 @pytest.mark.parametrize("fma,elide", [(True, 262144), (True, 1 << 62), (True, 16), (False, 262144)])
 def test_narrow_path_vs_oracle(monkeypatch, fma, elide):
-    """Matrices at most 8 entries wide take the narrow kernels (per-warp TMA
-    double buffer; ZK_NARROW=1 the direct variant, 0 the ring): ragged rows
-    with empty rows, whole empty slices, a partial last slice, both elision
-    orders and both product formulas -- every variant the oracle's bits, in
-    SpMV and in a BiCGStab solve (whose SpMV phases use the same kernels)."""
+    """Matrices at most 8 / 16 entries wide take the narrow kernels (per-warp
+    TMA double buffer; ZK_NARROW=0 the ring): ragged rows with empty rows,
+    whole empty slices, a partial last slice, both elision orders and both
+    product formulas -- every width class and the ring the oracle's bits, in
+    SpMV and in BiCGStab solves (whose SpMV phases, the two-vector one
+    included, use the same kernels)."""
     rng = np.random.default_rng(88)
     n = 70001  # partial last slice; > 16 warps x 2 CTAs x 148 SMs of slices
-    lens = rng.integers(0, 9, n)
-    lens[64:128] = 0  # two empty slices
-    lens[1000:1040] = 8
-    ia = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
-    ja = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int64)
-    aa = rng.standard_normal(ia[-1]) + 1j * rng.standard_normal(ia[-1])
-    x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
     Z.set_arithmetic(fma, elide)
     O.set_arith(fma, elide)
     try:
-        want = bits(O.spmv(n, n, ia, ja, aa, x))
-        for mode in ("2", "1", "0"):
-            monkeypatch.setenv("ZK_NARROW", mode)
-            A = Z.CsrMatrix(n, n, aa, ja, ia)
-            assert bits(Z.spmv(A, Z.ZVector(x)).data) == want, mode
+        for wmax in (8, 16):
+            lens = rng.integers(0, wmax + 1, n)
+            lens[64:128] = 0  # two empty slices
+            lens[1000:1040] = wmax
+            ia = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+            ja = np.concatenate([np.sort(rng.choice(n, L, replace=False)) for L in lens]).astype(np.int64)
+            aa = rng.standard_normal(ia[-1]) + 1j * rng.standard_normal(ia[-1])
+            x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+            want = bits(O.spmv(n, n, ia, ja, aa, x))
+            for mode in ("16", "8", "0"):
+                monkeypatch.setenv("ZK_NARROW", mode)
+                A = Z.CsrMatrix(n, n, aa, ja, ia)
+                assert bits(Z.spmv(A, Z.ZVector(x)).data) == want, (wmax, mode)
         monkeypatch.delenv("ZK_NARROW")
+        # a width-16 system through the solver (two-vector SpMV phase)
+        ia, ja, aa, b = _wide_dominant(3000, 9, 16, seed=5)
+        A = Z.CsrMatrix(3000, 3000, aa, ja, ia)
+        M = Z.build_jacobi(A)
+        xs, rep = Z.solve_bicgstab(A, Z.ZVector(b), M, Z.SolverConfig(tolerance=1e-10, max_iterations=200))
+        xo, hist, it, st, _ = O.bicgstab(3000, ia, ja, aa, b, M.data, None, 1e-10, 200)
+        assert rep.residual_history == hist and bits(xs.data) == bits(xo)
         # a diagonally dominant narrow system for the solver
         m, ia2, ja2, aa2, b = problems.helmholtz_fd(3, 33, frequency=33 / 12.0, damping=0.3)
         A = Z.CsrMatrix(m, m, aa2, ja2, ia2)
