@@ -7,7 +7,7 @@ python bench.py --steps 20 --warmup 5 > gpurun_out/r02_bench.json 2> gpurun_out/
 python __graft_entry__.py smoke > gpurun_out/r02_smoke.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/r02_launches.csv \
     python bench.py --steps 1 --warmup 1 --no-cpu --no-sweep --no-solvers > /dev/null 2>&1
-K='regex:k_spmv_phase|k_s_update_pipe|k_xr_update_pipe|k_tt_ts_pass|k_pivot_pass|k_res_pass|k_p_next|k_zdot_pipe|k_znorm2_pipe|k_spmv'
+K='regex:k_spmv2_phase_narrow|k_spmv_phase|k_s_update_pipe|k_xr_update_pipe|k_tt_ts_pass|k_pivot_pass|k_res_pass|k_p_next|k_zdot_pipe|k_znorm2_pipe|k_spmv'
 for c in C4 C5 C3 C1; do
   ZK_PROFILE_CONFIG=$c timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 12 \
       -o /tmp/r02_prof_$c python tools/profile_kernels.py > gpurun_out/r02_prof_$c.log 2>&1
