@@ -28,6 +28,16 @@ def test_library_exports_every_header_symbol():
     assert lib.zk_version().decode().endswith("sm_100a")
 
 
+def test_profile_phase_table_matches_header():
+    """zk_profile_read fills ZK_NPHASES entries in the order include/zk.h lists;
+    the Python table must have the same length (a mismatch reads past the
+    arrays or drops the narrow-matrix two-vector phase)."""
+    text = open(os.path.join(ROOT, "include", "zk.h")).read()
+    n = int(re.search(r"#define ZK_NPHASES (\d+)", text).group(1))
+    assert len(_lib.PHASES) == n
+    assert _lib.PHASES[-1] == "spmv2"
+
+
 def test_library_is_sm100a_cubin():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
