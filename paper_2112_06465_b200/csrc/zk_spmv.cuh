@@ -712,10 +712,10 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
 }
 
 // Persistent grid of a narrow launch (NX vectors).
+int num_sms();  // zk_internal.h (cached device attribute)
+
 __host__ __forceinline__ unsigned narrow_grid(const SellView& v, int nx = 1) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = num_sms();
     const int minb = v.narrow_w <= 8 ? (nx == 1 ? NarrowCfg<8>::kMinB : NarrowCfg<8>::kMinB2)
                                      : (nx == 1 ? NarrowCfg<16>::kMinB : NarrowCfg<16>::kMinB2);
     const int64_t want = (int64_t)sms * minb;

@@ -346,3 +346,25 @@ def test_narrow_path_vs_oracle(monkeypatch, fma, elide):
     finally:
         Z.set_arithmetic(True, 262144)
         O.set_arith(True, 262144)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_narrow_path_random_shapes(seed):
+    """Random small/odd shapes through the narrow kernels (n from 1 to a few
+    slices past a multiple of 32, rectangular, widths 0..16 with empty
+    slices), SpMV bitwise against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([1, 2, 31, 32, 33, 63, 65, 257, 1000, 4097, 5003, 40961]))
+    ncols = int(max(1, n + rng.integers(-min(n - 1, 5), 40)))
+    wmax = int(rng.choice([1, 3, 7, 8, 9, 12, 16]))
+    lens = rng.integers(0, wmax + 1, n)
+    if n > 64:
+        lens[32:64] = 0  # an empty slice in the middle
+    lens = np.minimum(lens, ncols)
+    ia = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    ja = (np.concatenate([np.sort(rng.choice(ncols, int(L), replace=False)) for L in lens])
+          if ia[-1] else np.zeros(0)).astype(np.int64)
+    aa = rng.standard_normal(ia[-1]) + 1j * rng.standard_normal(ia[-1])
+    x = rng.standard_normal(ncols) + 1j * rng.standard_normal(ncols)
+    A = Z.CsrMatrix(n, ncols, aa, ja, ia)
+    assert bits(Z.spmv(A, Z.ZVector(x)).data) == bits(O.spmv(n, ncols, ia, ja, aa, x)), (n, ncols, wmax)
