@@ -65,10 +65,11 @@ SellView sell_view(const zk_csr* A, const zk_context* c, size_t extra, int nsv) 
         v.spb = kBlock / kSlice;
         v.nvb = A->nblocks;
         {
-            // the x L2 bulk prefetch measured no gain on C4 and a 1.7% loss on C5
-            // (one more TMA op per slice): off unless ZK_PREFETCH=1
+            // the x L2 bulk prefetch (one more TMA op per slice): C4 SpMV 731 -> 724 us
+            // (three A/B pairs, +0.7% solves/s); it cost C5 1.7% when C5's 7-wide rows
+            // still ran on the ring (they take the narrow kernels now).  ZK_PREFETCH=0: off
             const char* e = std::getenv("ZK_PREFETCH");
-            v.prefetch = e && e[0] == '1';
+            v.prefetch = !(e && e[0] == '0');
         }
         return v;
     }
