@@ -152,6 +152,18 @@ struct KPlainBody {
     __device__ void finish(const double*) {}
 };
 
+// Two products from one matrix pass (narrow matrices, TFQMR): y0 = A x0, y1 = A x1.
+struct KPlain2Body {
+    static constexpr int kNC = 0, kNR = 0, kSV = 0;
+    double2* y0;
+    double2* y1;
+    __device__ __forceinline__ void row(int64_t r, const double2 (&v)[2], const double2 (&)[1], double2 (&)[1],
+                                        double (&)[1]) {
+        y0[r] = v[0];
+        y1[r] = v[1];
+    }
+};
+
 // _Run.true_relative_residual (krylov.py:183-186) and what the caller does with it:
 //   MODE 0  BiCGSTAB(l) residual probe (krylov.py:355-360): record + stop only when converged
 //   MODE 1  BiCGSTAB(l) end of cycle (krylov.py:403-407): record; stop when converged or at the cap
@@ -223,6 +235,15 @@ __global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
     extern __shared__ __align__(128) unsigned char smem[];
     if (gate.skip()) return;
     narrow_tma_run<WM, 1>(A, x, x, body, smem);
+}
+
+template <int WM>
+__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB2)
+    k_kspmv2_narrow(SellView A, const double2* __restrict__ x0, const double2* __restrict__ x1, KPlain2Body body,
+                    Gate gate) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    if (gate.skip()) return;
+    narrow_tma_run<WM, 2>(A, x0, x1, body, smem);
 }
 
 // ---- elementwise kernels -------------------------------------------------------
@@ -532,6 +553,7 @@ struct KLaunch {
     double* slots;
     int64_t count = 0;  // kernels enqueued
     cudaStream_t s;
+    bool fuse2 = false;  // narrow matrix: TFQMR's A x and A z in one pass (t_iteration)
 
     Gate live() const { return Gate{&P->st->done, Gate::kLive}; }
     Gate nofl() const { return Gate{&P->st->done, Gate::kLiveNoFlag}; }
@@ -604,9 +626,22 @@ struct KLaunch {
         k_pairs<<<ew, kEwThreads, 0, s>>>(p, n, fma, g);
         check();
     }
+    // y0 = A x0 and y1 = A x1 in one pass over a narrow matrix
+    void spmv2(const double2* x0, const double2* x1, double2* y0, double2* y1, Gate g) {
+        SellView v = sell_view(A, c, 0, 0);
+        plain_grid(A, v);
+        if (!v.narrow_w) throw ZkError{ZK_ERR_CUDA, "internal: two-vector SpMV needs a narrow matrix"};
+        ZK_NARROW_ATTR(k_kspmv2_narrow);
+        ZK_NARROW_LAUNCH(k_kspmv2_narrow, v, 2, s, v, x0, x1, KPlain2Body{y0, y1}, g);
+        check();
+    }
     template <int MODE>
     void true_res(Gate g) {  // A x into ax, then the residual pass (as the BiCGStab loop does)
         spmv(P->x, P->ax, nullptr, g);
+        res_pass<MODE>(g);
+    }
+    template <int MODE>
+    void res_pass(Gate g) {  // the residual pass over (b, ax)
         const double2* in[2] = {P->b, P->ax};
         const int8_t alias[2] = {0, 0};
         L1View v;
@@ -708,11 +743,13 @@ void t_iteration(KLaunch& L, int p) {
     for (int half = 0; half < 2; ++half) {
         const Gate g = half == 0 ? G : H;
         if (half == 1) {
-            Pairs py{};
-            add_pair(py, P->v, P->y, nullptr, &st->alpha, PF_NEG_B);
-            L.pairs(py, g);                          // y -= alpha v
-            if (P->jacobi) L.jac(P->y, P->z, g);     // z = M y
-            L.spmv(P->z, Uc, nullptr, g);            // uvec = A z
+            if (!L.fuse2) {
+                Pairs py{};
+                add_pair(py, P->v, P->y, nullptr, &st->alpha, PF_NEG_B);
+                L.pairs(py, g);                          // y -= alpha v
+                if (P->jacobi) L.jac(P->y, P->z, g);     // z = M y
+                L.spmv(P->z, Uc, nullptr, g);            // uvec = A z
+            }
             L.scalar(KO_T_COEFD, 0, 0, g);
         }
         Pairs pw{};
@@ -724,7 +761,20 @@ void t_iteration(KLaunch& L, int p) {
         Pairs px{};
         add_pair(px, P->d, P->x, nullptr, &st->eta, 0);                      // x += eta d
         L.pairs(px, g);
-        L.true_res<2>(g);
+        if (half == 0 && L.fuse2) {
+            // narrow matrix: the second half-step's y, z updates move ahead of the
+            // first half-step's residual (they read v, alpha and y only; if the
+            // residual converges they are dead, as in the reference's break), so
+            // A x and the second half-step's A z share one matrix pass
+            Pairs py{};
+            add_pair(py, P->v, P->y, nullptr, &st->alpha, PF_NEG_B);
+            L.pairs(py, g);                          // y -= alpha v
+            if (P->jacobi) L.jac(P->y, P->z, g);     // z = M y
+            L.spmv2(P->x, P->z, P->ax, Uc, g);       // A x (residual), uvec = A z
+            L.res_pass<2>(g);
+        } else {
+            L.true_res<2>(g);
+        }
     }
     k_krecord<<<1, 1, 0, L.s>>>(st, P->hist, G);
     L.check();
@@ -819,6 +869,13 @@ static void build_kgraph(zk_context* c, const zk_csr* A, KrylovPlan* P) {
     const int64_t cap = (int64_t)num_sms() * 8;
     L.ew = (unsigned)(ewg < 1 ? 1 : (ewg > cap ? cap : ewg));
     L.pg = pipe_grid(A);
+    {
+        // ZK_FUSE2=0: no two-vector SpMV (A/B)
+        SellView v = sell_view(A, c, 0, 0);
+        plain_grid(A, v);
+        const char* e = std::getenv("ZK_FUSE2");
+        L.fuse2 = v.narrow_w != 0 && !(e && e[0] == '0');
+    }
     // everything that may allocate or upload happens before the capture
     L.pc = c->plans_for(P->n, kBlock, kComplex);
     L.pr = c->plans_for(P->n, kBlock, kReal);
