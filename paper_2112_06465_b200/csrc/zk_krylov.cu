@@ -57,6 +57,7 @@ struct KState {
     int64_t maxit, iterations, trips;
     double b_norm, tol, r0_norm, rel, theta, tau, c, nrm;
     double2 rho, alpha, omega, beta, eta, coefd, dot;
+    double2 rho_prev;  // TFQMR, narrow matrices: rho before KO_T_BETA_CALC (its check is deferred)
 };
 
 // MR scalars of BiCGSTAB(l), indexed as in krylov.py:366-391 (l <= kMaxEll).
@@ -403,6 +404,9 @@ enum KOp : int32_t {
     KO_T_THETA = 12,  // tau check; theta, c, tau, eta                   (krylov.py:454-459)
     KO_T_BETA = 14,   // rho check; beta = rho'/rho; rho = rho'           (krylov.py:469-473)
     KO_T_END = 15,    // iteration cap                                   (krylov.py:438)
+    // TFQMR with the end-of-iteration products moved ahead of the second residual
+    KO_T_BETA_CALC = 16,  // beta = rho'/rho; rho = rho' (rho kept for the check)  (krylov.py:471-473)
+    KO_T_BETA_CHK = 17,   // rho check, in the reference's place after record     (krylov.py:469-470)
 };
 
 __global__ void k_kscalar(KState* st, KMr* mr, int32_t op, int32_t i, int32_t j, Gate gate) {
@@ -489,6 +493,14 @@ __global__ void k_kscalar(KState* st, KMr* mr, int32_t op, int32_t i, int32_t j,
             st->rho = rn;
             return;
         }
+        case KO_T_BETA_CALC:
+            st->rho_prev = st->rho;
+            st->beta = cdiv_py(st->dot, st->rho);
+            st->rho = st->dot;
+            return;
+        case KO_T_BETA_CHK:
+            if (small_py(st->rho_prev)) kstop(st, KS_BREAKDOWN, KB_RHO);
+            return;
         case KO_T_END:
             if (st->iterations >= st->maxit) kstop(st, KS_NOT_CONVERGED);
             return;
@@ -761,7 +773,19 @@ void t_iteration(KLaunch& L, int p) {
         Pairs px{};
         add_pair(px, P->d, P->x, nullptr, &st->eta, 0);                      // x += eta d
         L.pairs(px, g);
-        if (half == 0 && L.fuse2) {
+        if (half == 1 && L.fuse2) {
+            // ... and the end of the iteration's rho', beta, y, z ahead of the
+            // second residual (the rho check stays after the record, below), so
+            // A x and the next uvec = A z share one pass too
+            L.dot(P->rs, P->w, g);  // rho'
+            L.scalar(KO_T_BETA_CALC, 0, 0, g);
+            Pairs py{};
+            add_pair(py, P->w, P->y, &st->beta, nullptr, PF_SCALE);          // y = y * beta + w
+            L.pairs(py, g);
+            if (P->jacobi) L.jac(P->y, P->z, g);
+            L.spmv2(P->x, P->z, P->ax, Un, g);       // A x (residual), uvec' = A M^-1 y
+            L.res_pass<2>(g);
+        } else if (half == 0 && L.fuse2) {
             // narrow matrix: the second half-step's y, z updates move ahead of the
             // first half-step's residual (they read v, alpha and y only; if the
             // residual converges they are dead, as in the reference's break), so
@@ -778,13 +802,17 @@ void t_iteration(KLaunch& L, int p) {
     }
     k_krecord<<<1, 1, 0, L.s>>>(st, P->hist, G);
     L.check();
-    L.dot(P->rs, P->w, G);  // rho'
-    L.scalar(KO_T_BETA, 0, 0, G);
-    Pairs py{};
-    add_pair(py, P->w, P->y, &st->beta, nullptr, PF_SCALE);                  // y = y * beta + w
-    L.pairs(py, G);
-    if (P->jacobi) L.jac(P->y, P->z, G);
-    L.spmv(P->z, Un, nullptr, G);                                            // uvec' = A M^-1 y
+    if (L.fuse2) {
+        L.scalar(KO_T_BETA_CHK, 0, 0, G);
+    } else {
+        L.dot(P->rs, P->w, G);  // rho'
+        L.scalar(KO_T_BETA, 0, 0, G);
+        Pairs py{};
+        add_pair(py, P->w, P->y, &st->beta, nullptr, PF_SCALE);              // y = y * beta + w
+        L.pairs(py, G);
+        if (P->jacobi) L.jac(P->y, P->z, G);
+        L.spmv(P->z, Un, nullptr, G);                                        // uvec' = A M^-1 y
+    }
     k_tf_v<<<L.ew, kEwThreads, 0, L.s>>>(L.n, P->v, Uc, Un, st, L.fma, G);
     L.check();
     L.scalar(KO_T_END, 0, 0, G);

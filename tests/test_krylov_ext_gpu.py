@@ -83,3 +83,35 @@ def test_device_driver_one_launch_per_solve():
     M = Z.Preconditioner("jacobi", g["minv"])
     x, rep = Z.solve_bicgstab_l(A, Z.ZVector(g["b"].copy()), M, Z.SolverConfig(tolerance=1e-9, l=8))
     assert rep.kernel_launches > 100  # the whole cycle ran on the device
+
+
+# Small systems on which TFQMR breaks down (found by a seeded search with the
+# oracle): rho after 39 / 43 iterations -- the check the narrow-matrix loop
+# defers past the record -- and sigma, alpha, quasi-residual tau after
+# several iterations.  (n, rows as {col: value}, b, expected breakdown name)
+_TFQMR_BREAKDOWNS = [
+    (3, [{0: 2, 2: 1}, {2: 1}, {0: 1j, 2: 2}], [-1, 0, 1], "rho"),
+    (4, [{0: 0.5, 3: 2}, {3: -1}, {1: 0.5, 3: 1j}, {1: 2, 3: -1}], [0, 1j, 0, 1], "rho"),
+    (3, [{0: 0.5, 1: 1}, {0: 1j}, {1: 0.5}], [-1, 1, 0], "sigma = <r~, v>"),
+    (5, [{2: 2, 4: 0.5}, {1: 1j, 2: 1, 4: 1j}, {0: -1, 1: -1, 3: 1j, 4: 1j}, {4: 1}, {0: -1j, 1: 1j}],
+     [1j, 0, 1, 0, 0], "alpha"),
+    (4, [{2: -1j}, {1: 0.5}, {2: 2}, {0: -1, 1: -1j}], [0, 1, 0, 1], "quasi-residual tau"),
+]
+
+
+@pytest.mark.parametrize("case", range(len(_TFQMR_BREAKDOWNS)))
+def test_tfqmr_breakdowns_vs_oracle(case):
+    from oracle import oracle as O
+    O.set_arith(True, 262144)
+    n, rows, b, name = _TFQMR_BREAKDOWNS[case]
+    ia = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    ja = np.array([c for r in rows for c in sorted(r)], dtype=np.int64)
+    aa = np.array([r[c] for r in rows for c in sorted(r)], dtype=np.complex128)
+    b = np.array(b, dtype=np.complex128)
+    xo, hist, it, st, what = O.tfqmr(n, ia, ja, aa, b, None, None, 1e-12, 50)
+    assert st == 2 and O.EXT_BREAKDOWN_NAMES[what] == name, (st, what)
+    A = Z.CsrMatrix(n, n, aa, ja, ia)
+    with pytest.raises(Z.BreakdownError) as e:
+        Z.solve_tfqmr(A, Z.ZVector(b), Z.Preconditioner.identity(), Z.SolverConfig(tolerance=1e-12, max_iterations=50))
+    assert str(e.value) == O.breakdown_message(what, 0, it, ext=True)
+    assert e.value.report.residual_history == hist
