@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spmv_phase(SellView A, cons
 }
 
 template <int WM>
-__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
+__global__ void __launch_bounds__(32 * NarrowCfg<WM>::warps(1), NarrowCfg<WM>::kMinB)
     k_spmv_phase_narrow(SellView A, const double2* __restrict__ x, double2* __restrict__ y, const SolverState* st) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (st->done) return;
@@ -236,7 +236,7 @@ struct PhaseSpmv2Body {
 };
 
 template <int WM>
-__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB2)
+__global__ void __launch_bounds__(32 * NarrowCfg<WM>::warps(2), NarrowCfg<WM>::kMinB2)
     k_spmv2_phase_narrow(SellView A, const double2* __restrict__ x0, const double2* __restrict__ x1,
                          double2* __restrict__ y0, double2* __restrict__ y1, const SolverState* st) {
     extern __shared__ __align__(128) unsigned char smem[];

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_kspmv(SellView A, const dou
 }
 
 template <int WM>
-__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
+__global__ void __launch_bounds__(32 * NarrowCfg<WM>::warps(1), NarrowCfg<WM>::kMinB)
     k_kspmv_narrow(SellView A, const double2* __restrict__ x, KPlainBody body, Gate gate) {
     extern __shared__ __align__(128) unsigned char smem[];
     if (gate.skip()) return;
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
 }
 
 template <int WM>
-__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB2)
+__global__ void __launch_bounds__(32 * NarrowCfg<WM>::warps(2), NarrowCfg<WM>::kMinB2)
     k_kspmv2_narrow(SellView A, const double2* __restrict__ x0, const double2* __restrict__ x1, KPlain2Body body,
                     Gate gate) {
     extern __shared__ __align__(128) unsigned char smem[];

@@ -235,7 +235,7 @@ struct PlainSpmv {
 };
 
 template <int WM>
-__global__ void __launch_bounds__(kNarrowThreads, NarrowCfg<WM>::kMinB)
+__global__ void __launch_bounds__(32 * NarrowCfg<WM>::warps(1), NarrowCfg<WM>::kMinB)
     k_spmv_narrow(SellView A, const double2* __restrict__ x, double2* __restrict__ y) {
     extern __shared__ __align__(128) unsigned char smem[];
     PlainSpmv body{y};

@@ -608,10 +608,17 @@ constexpr int kNarrowWarps = kNarrowThreads / 32;
 #ifndef ZK_NARROW2_MINB
 #define ZK_NARROW2_MINB 2  // width 8, two vectors: 128 registers, no spills (1 CTA at 144: 857 vs 589 us on C5)
 #endif
+#ifndef ZK_NARROW16_WARPS
+#define ZK_NARROW16_WARPS 12  // width 16, one vector: warps per CTA (148 registers: 12 fit one SM)
+#endif
 template <int WM>
 struct NarrowCfg {
     static constexpr int kStage = WM * kSlice * 16;  // values of one slice
-    static constexpr int kSmem = 128 + kNarrowWarps * 2 * kStage;
+    // warps per CTA: 8, except width 16 with one vector (one CTA per SM)
+    static constexpr int warps(int nx) { return (WM > 8 && nx == 1) ? ZK_NARROW16_WARPS : kNarrowWarps; }
+    static constexpr int kBars = 256;  // two mbarriers per warp, up to 16 warps
+    static constexpr int smem(int nx) { return kBars + warps(nx) * 2 * kStage; }
+    static constexpr int kSmem = smem(1) > smem(2) ? smem(1) : smem(2);  // attribute for either
     static constexpr int kMinB = WM <= 8 ? ZK_NARROW_MINB : 1;    // one vector
     static constexpr int kMinB2 = WM <= 8 ? ZK_NARROW2_MINB : 1;  // two vectors
 };
@@ -623,11 +630,13 @@ __device__ __forceinline__ void narrow_tma_run(const SellView& A, const double2*
                                                const double2* __restrict__ x1, Body& body, unsigned char* smem) {
     static_assert(Body::kSV == 0 && Body::kNC == 0 && Body::kNR == 0, "plain bodies only");
     constexpr int kStage = NarrowCfg<WM>::kStage;
+    constexpr int kW = NarrowCfg<WM>::warps(NX);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + 2 * warp;
-    unsigned char* buf = smem + 128 + (size_t)warp * 2 * kStage;
-    const int64_t ns = A.nslices, nw = (int64_t)gridDim.x * kNarrowWarps;
-    int64_t s = (int64_t)blockIdx.x * kNarrowWarps + warp;
+    static_assert(kW * 2 * 8 <= NarrowCfg<WM>::kBars, "mbarrier area");
+    unsigned char* buf = smem + NarrowCfg<WM>::kBars + (size_t)warp * 2 * kStage;
+    const int64_t ns = A.nslices, nw = (int64_t)gridDim.x * kW;
+    int64_t s = (int64_t)blockIdx.x * kW + warp;
     if (s >= ns) return;
     if (lane == 0) {
         mbar_init(&bar[0], 1);
@@ -719,20 +728,21 @@ __host__ __forceinline__ unsigned narrow_grid(const SellView& v, int nx = 1) {
     const int minb = v.narrow_w <= 8 ? (nx == 1 ? NarrowCfg<8>::kMinB : NarrowCfg<8>::kMinB2)
                                      : (nx == 1 ? NarrowCfg<16>::kMinB : NarrowCfg<16>::kMinB2);
     const int64_t want = (int64_t)sms * minb;
-    const int64_t need = (v.nslices + kNarrowWarps - 1) / kNarrowWarps;
+    const int w = v.narrow_w <= 8 ? NarrowCfg<8>::warps(nx) : NarrowCfg<16>::warps(nx);
+    const int64_t need = (v.nslices + w - 1) / w;
     return (unsigned)(need < want ? (need > 0 ? need : 1) : want);
 }
-__host__ __forceinline__ size_t narrow_smem(const SellView& v) {
-    return v.narrow_w <= 8 ? NarrowCfg<8>::kSmem : NarrowCfg<16>::kSmem;
+__host__ __forceinline__ size_t narrow_smem(const SellView& v, int nx = 1) {
+    return v.narrow_w <= 8 ? NarrowCfg<8>::smem(nx) : NarrowCfg<16>::smem(nx);
 }
 
 // Launch kernel template KERN<8> or KERN<16> by the view's narrow width.
 #define ZK_NARROW_LAUNCH(KERN, V, NX, STREAM, ...)                                                         \
     do {                                                                                                  \
         if ((V).narrow_w <= 8)                                                                            \
-            KERN<8><<<narrow_grid((V), (NX)), kNarrowThreads, narrow_smem(V), (STREAM)>>>(__VA_ARGS__);  \
+            KERN<8><<<narrow_grid((V), (NX)), 32 * NarrowCfg<8>::warps(NX), narrow_smem((V), (NX)), (STREAM)>>>(__VA_ARGS__); \
         else                                                                                              \
-            KERN<16><<<narrow_grid((V), (NX)), kNarrowThreads, narrow_smem(V), (STREAM)>>>(__VA_ARGS__); \
+            KERN<16><<<narrow_grid((V), (NX)), 32 * NarrowCfg<16>::warps(NX), narrow_smem((V), (NX)), (STREAM)>>>(__VA_ARGS__); \
     } while (0)
 // Dynamic shared memory attributes of both instantiations.
 #define ZK_NARROW_ATTR(KERN)                                                                                     \
