@@ -110,14 +110,20 @@ unsigned pipe_grid(const zk_csr* A) {
 }
 
 // Plain (reduction-free) SpMV launches: pipeline blocks of v.spb slices --
-// 128 (the 4096-row block) for large matrices, fewer when the matrix has
-// fewer blocks than two per SM, so every SM streams -- and its grid.
+// 16 (512 rows) for large matrices, fewer when the matrix has fewer blocks
+// than two per SM, so every SM streams -- and its grid.
 unsigned plain_grid(const zk_csr* A, SellView& v) {
     const int64_t want = 2 * (int64_t)num_sms();
-    int64_t spb = kBlock / kSlice;
+    // 16 slices (512 rows) per pipeline block: a finer last wave than the
+    // 4096-row reduction block (C4 SpMV 712 -> 704 us; 32 slices: 707)
+    int64_t spb = 16;
     if (A->nslices < want * spb) {
         spb = (A->nslices + want - 1) / want;
         if (spb < 4) spb = 4;
+    }
+    if (const char* e = std::getenv("ZK_SPB")) {  // experiments: pipeline block size in slices
+        const int64_t f = std::atoll(e);
+        if (f >= 1 && f < spb) spb = f;
     }
     v.spb = (int32_t)spb;
     v.nvb = (A->nslices + spb - 1) / spb;
